@@ -1,0 +1,259 @@
+"""CPU oracle for the ILS smoothing hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is a numpy/scipy restatement of the reference's algorithm
+(ilsmooth, /root/reference/pkg/src/ilsmooth) for the one path this repo
+accelerates: smooth_plane / smooth_color with the ILS loop
+(Algorithm 1).  It exists to CHECK the CUDA product:
+
+  * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+    --impl reference leg may import it;
+  * the product package (paper_2003_07504_b200) never imports it and has
+    no CPU fallback -- it raises if the CUDA library is missing.
+
+Parity is pinned (not just asserted): tests/test_oracle_golden.py checks
+this file against golden vectors produced by importing the real reference
+(tests/golden/make_golden.py, committed together with its outputs) and
+against the reference's own frozen values and its committed 30-iteration
+energy trace (pkg/demos/out/energy_trace.csv).
+
+Every function cites the reference file:line it restates.  The FFT goes
+through scipy.fft exactly as the reference does (solver.py:24-30), so the
+restatement is bitwise-faithful on the same SciPy build.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.fft as _sfft
+
+DEFAULT_EPS = 1e-4  # penalty.py:40
+_CURVATURE_SLACK = 1e-12  # penalty.py:44
+
+
+# ---------------------------------------------------------------- penalties
+class Charbonnier:
+    """penalty.py:47-75: (x^2+eps)^(p/2)."""
+
+    def __init__(self, p=0.8, eps=DEFAULT_EPS):
+        if not (0.0 < p <= 1.0):  # penalty.py:54-56
+            raise ValueError("p must be in (0,1]")
+        if not (eps > 0.0):  # penalty.py:57-58
+            raise ValueError(f"eps must be positive, got {eps}")
+        self.p, self.eps = float(p), float(eps)
+
+    def value(self, x):  # penalty.py:60-62
+        x = np.asarray(x, dtype=np.float64)
+        return (x * x + self.eps) ** (self.p / 2.0)
+
+    def derivative(self, x):  # penalty.py:64-66
+        x = np.asarray(x, dtype=np.float64)
+        return self.p * x * (x * x + self.eps) ** (self.p / 2.0 - 1.0)
+
+    def edge_stop(self, x):  # penalty.py:68-70
+        x = np.asarray(x, dtype=np.float64)
+        return (self.p / 2.0) * (x * x + self.eps) ** (self.p / 2.0 - 1.0)
+
+    @property
+    def min_curvature(self):  # penalty.py:72-75
+        return self.p * self.eps ** (self.p / 2.0 - 1.0)
+
+
+class Welsch:
+    """penalty.py:78-105: 2 g^2 (1 - exp(-x^2 / 2g^2))."""
+
+    def __init__(self, gamma):
+        if not (gamma > 0.0):  # penalty.py:84-86
+            raise ValueError(f"gamma must be positive, got {gamma}")
+        self.gamma = float(gamma)
+
+    def value(self, x):  # penalty.py:88-91
+        x = np.asarray(x, dtype=np.float64)
+        g2 = self.gamma * self.gamma
+        return 2.0 * g2 * (1.0 - np.exp(-x * x / (2.0 * g2)))
+
+    def derivative(self, x):  # penalty.py:93-96
+        x = np.asarray(x, dtype=np.float64)
+        g2 = self.gamma * self.gamma
+        return 2.0 * x * np.exp(-x * x / (2.0 * g2))
+
+    def edge_stop(self, x):  # penalty.py:98-101
+        x = np.asarray(x, dtype=np.float64)
+        g2 = self.gamma * self.gamma
+        return np.exp(-x * x / (2.0 * g2))
+
+    @property
+    def min_curvature(self):  # penalty.py:103-105
+        return 2.0
+
+
+def check_curvature(spec, c):
+    """penalty.py:108-114."""
+    c0 = spec.min_curvature
+    if not np.isfinite(c) or c < c0 * (1.0 - _CURVATURE_SLACK):
+        raise ValueError(f"curvature c={c} is below the minimum {c0}")
+
+
+def aux_update(spec, c, x):
+    """penalty.py:117-126: mu = c*x - phi'(x)."""
+    check_curvature(spec, c)
+    x = np.asarray(x, dtype=np.float64)
+    return c * x - spec.derivative(x)
+
+
+# ---------------------------------------------------------------- operators
+def grad_x(u):
+    """solver.py:33-35: periodic forward difference along axis 1."""
+    return np.roll(u, -1, axis=1) - u
+
+
+def grad_y(u):
+    """solver.py:38-40: periodic forward difference along axis 0."""
+    return np.roll(u, -1, axis=0) - u
+
+
+def adjoint_accumulate(mu_x, mu_y):
+    """solver.py:43-49: Dx^T mu_x + Dy^T mu_y (periodic)."""
+    if mu_x.shape != mu_y.shape:
+        raise ValueError(f"field shapes differ: {mu_x.shape} vs {mu_y.shape}")
+    return np.roll(mu_x, 1, axis=1) - mu_x + np.roll(mu_y, 1, axis=0) - mu_y
+
+
+def denominator(height, width, lam, c):
+    """solver.py:100-102: 1 + (c lam / 2)(wy + wx), w = 2 - 2cos(2 pi k / n)."""
+    wx = 2.0 - 2.0 * np.cos(2.0 * np.pi * np.arange(width) / width)
+    wy = 2.0 - 2.0 * np.cos(2.0 * np.pi * np.arange(height) / height)
+    return 1.0 + (c * lam / 2.0) * (wy[:, None] + wx[None, :])
+
+
+def solve_ls(f, mu_x, mu_y, lam, c, workers=1, f_hat=None, denom=None):
+    """solver.py:109-134: u = ifft2((fft2(f) + lam/2 fft2(D^T mu)) / denom).real."""
+    h, w = f.shape
+    if denom is None:
+        denom = denominator(h, w, lam, c)
+    if f_hat is None:
+        f_hat = _sfft.fft2(f, workers=workers)
+    rhs_hat = f_hat + (lam / 2.0) * _sfft.fft2(adjoint_accumulate(mu_x, mu_y), workers=workers)
+    u = _sfft.ifft2(rhs_hat / denom, workers=workers)
+    return np.ascontiguousarray(u.real)
+
+
+def dense_solve(f, mu_x, mu_y, lam, c):
+    """solver.py:152-179 restated with dense numpy matrices (<= 4096 px)."""
+    h, w = f.shape
+    n = h * w
+    if n > 4096:
+        raise ValueError("dense oracle refuses > 4096 pixels")
+
+    def cyc(m):
+        d = -np.eye(m)
+        d[np.arange(m), (np.arange(m) + 1) % m] += 1.0
+        return d
+
+    dx = np.kron(np.eye(h), cyc(w))
+    dy = np.kron(cyc(h), np.eye(w))
+    a = np.eye(n) + (c * lam / 2.0) * (dx.T @ dx + dy.T @ dy)
+    rhs = f.ravel() + (lam / 2.0) * (dx.T @ mu_x.ravel() + dy.T @ mu_y.ravel())
+    return np.linalg.solve(a, rhs).reshape(h, w)
+
+
+# ---------------------------------------------------------------- smoother
+def energy(u, f, spec, lam):
+    """smoother.py:93-101."""
+    d = u - f
+    return float(
+        np.sum(d * d)
+        + lam * (np.sum(spec.value(grad_x(u))) + np.sum(spec.value(grad_y(u))))
+    )
+
+
+def smooth_plane(f, spec, lam, iters=4, c=None, trace=False, workers=1):
+    """smoother.py:132-172 (plan built per call, solver.py:78-106)."""
+    f = np.asarray(f, dtype=np.float64)
+    c = spec.min_curvature if c is None else float(c)
+    h, w = f.shape
+    denom = denominator(h, w, lam, c)
+    f_hat = _sfft.fft2(f, workers=workers)  # SolverPlan.with_data, solver.py:69-75
+    u = f
+    energies = [energy(u, f, spec, lam)] if trace else None
+    for n in range(iters):  # smoother.py:162-169
+        mx = aux_update(spec, c, grad_x(u))
+        my = aux_update(spec, c, grad_y(u))
+        u = solve_ls(f, mx, my, lam, c, workers, f_hat=f_hat, denom=denom)
+        if not np.all(np.isfinite(u)):
+            raise ArithmeticError(f"non-finite iterate at iteration {n + 1}")
+        if trace:
+            energies.append(energy(u, f, spec, lam))
+    return (u, energies) if trace else u
+
+
+def rgb_to_yuv(r, g, b):
+    """image.py:110-117 (BT.601)."""
+    y = 0.299 * r + 0.587 * g + 0.114 * b
+    return y, 0.492 * (b - y), 0.877 * (r - y)
+
+
+def yuv_to_rgb(y, u, v):
+    """image.py:120-128."""
+    r = y + v / 0.877
+    b = y + u / 0.492
+    g = (y - 0.299 * r - 0.114 * b) / 0.587
+    return r, g, b
+
+
+def smooth_color(planes, spec, lam, iters=4, c=None, luminance_only=False, trace=False, workers=1):
+    """smoother.py:175-217 for gray (1 plane) or rgb (3 planes) input.
+
+    Per-channel RGB shares one plan (smoother.py:203-212); traced energies
+    are summed across channels (213-216).  luminance_only smooths Y of the
+    BT.601 decomposition and passes chroma through (195-202).
+    """
+    planes = [np.asarray(p, dtype=np.float64) for p in planes]
+    if len(planes) == 3 and luminance_only:
+        y, cu, cv = rgb_to_yuv(*planes)
+        res = smooth_plane(y, spec, lam, iters, c, trace, workers)
+        ys = res[0] if trace else res
+        out = list(yuv_to_rgb(ys, cu, cv))
+        return (out, res[1]) if trace else out
+    results = [smooth_plane(p, spec, lam, iters, c, trace, workers) for p in planes]
+    if trace:
+        outs = [r[0] for r in results]
+        summed = [float(sum(v)) for v in zip(*(r[1] for r in results))]
+        return outs, summed
+    return results
+
+
+# ---------------------------------------------------------------- fixtures
+def bench_planes(height, width, channels, seed=20240607):
+    """The reference bench inputs: cli.py:270-273 (rng.random per plane)."""
+    rng = np.random.default_rng(seed)
+    return [rng.random((height, width)) for _ in range(channels)]
+
+
+def make_photo(h=192, w=192, seed=3):
+    """Restates demos/energy_trace.py:20-29 (the golden-trace input)."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:h, 0:w] / h
+    img = 0.35 + 0.25 * (xx + yy < 0.9)
+    for _ in range(6):
+        cy, cx, r = rng.random(3) * (0.8, 0.8, 0.15) + (0.1, 0.1, 0.04)
+        img += 0.2 * np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / r**2)
+    img += 0.02 * rng.standard_normal((h, w))
+    return np.clip(img, 0.0, 1.0)
+
+
+def make_test_card(h=192, w=256, seed=7):
+    """Restates demos/smooth_basics.py:22-31."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:h, 0:w]
+    img = np.full((h, w), 0.25)
+    img[20:90, 20:110] = 0.8
+    img[(yy - 130) ** 2 + (xx - 70) ** 2 <= 35**2] = 0.55
+    img[30:80, 130:240] += 0.3 * (xx[30:80, 130:240] - 130) / 110
+    img[110:180, 130:240] += 0.08 * np.sin(xx[110:180, 130:240] * 1.1)
+    img += 0.03 * rng.standard_normal((h, w))
+    return np.clip(img, 0.0, 1.0)
+
+
+def psnr(a, b, peak=1.0):
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return float("inf") if mse == 0.0 else 10.0 * np.log10(peak * peak / mse)

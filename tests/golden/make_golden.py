@@ -1,0 +1,97 @@
+"""Generate golden vectors by running the REAL reference (ilsmooth) in-process.
+
+Run in the build container only (needs /root/reference, read-only):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes tests/golden/golden.npz.  The GPU box never runs this script; the
+committed .npz travels with the repo.  Inputs are stored alongside the
+outputs so the fixtures do not depend on numpy's RNG stream staying put.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from dataclasses import replace
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import ilsmooth as ref  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+
+
+def main():
+    g = {}
+    # --- solve_ls vs the reference (test_solver.py:78-88 shapes + a few more)
+    solver_shapes = [(4, 4), (5, 7), (16, 16), (17, 13), (1, 6), (3, 1), (9, 11), (20, 14), (32, 24), (12, 10)]
+    rng = np.random.default_rng(42)
+    for i, (h, w) in enumerate(solver_shapes):
+        for j, (lam, c) in enumerate(((0.1, 2.0), (1.0, 100.0), (10.0, 2.0))):
+            f = rng.standard_normal((h, w))
+            mx = rng.standard_normal((h, w))
+            my = rng.standard_normal((h, w))
+            u = ref.solve_ls(ref.make_plan(h, w, lam, c, f), f, mx, my)
+            k = f"solve_{i}_{j}"
+            g[k + "_f"], g[k + "_mx"], g[k + "_my"], g[k + "_u"] = f, mx, my, u
+            g[k + "_lamc"] = np.array([lam, c])
+
+    # --- smooth_plane (Charbonnier / Welsch), smoother.py:132-172
+    cases = [
+        ("sp_uniform_18x22", np.random.default_rng(5).random((18, 22)), ref.Charbonnier(0.8, 1e-4), 1.0, 4, None),
+        ("sp_uniform_64x80", np.random.default_rng(11).random((64, 80)), ref.Charbonnier(0.8, 1e-4), 1.0, 4, None),
+        ("sp_welsch_20x20", np.random.default_rng(10).random((20, 20)), ref.Welsch(0.1), 2.0, 5, None),
+        ("sp_p05_c4_48x40", np.random.default_rng(12).random((48, 40)), ref.Charbonnier(0.5, 1e-3), 3.0, 6, 4.0 * ref.Charbonnier(0.5, 1e-3).min_curvature),
+        ("sp_odd_33x45", np.random.default_rng(13).random((33, 45)), ref.Charbonnier(0.8, 1e-4), 1.0, 4, None),
+        ("sp_prime_17x13", np.random.default_rng(14).random((17, 13)), ref.Charbonnier(1.0, 1e-4), 0.5, 3, None),
+        ("sp_card_192x256", None, ref.Charbonnier(0.8, 1e-4), 1.0, 4, None),
+        ("sp_texture_welsch_60x45", np.random.default_rng(15).random((60, 45)), ref.Welsch(10 / 255), 30.0, 10, 2.0),
+    ]
+    for name, f, pen, lam, iters, c in cases:
+        if f is None:
+            import importlib.util
+            spec = importlib.util.spec_from_file_location("sb", "/root/reference/pkg/demos/smooth_basics.py")
+            sb = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(sb)
+            f = sb.make_test_card()
+        params = ref.SmoothParams(pen, lam, iters=iters, c=c)
+        u, tr = ref.smooth_plane(f, params, trace=True)
+        g[name + "_f"] = f
+        g[name + "_u"] = u
+        g[name + "_energies"] = np.array(tr.energies)
+        if isinstance(pen, ref.Charbonnier):
+            g[name + "_pen"] = np.array([0, pen.p, pen.eps, 0.0, lam, params.curvature, iters])
+        else:
+            g[name + "_pen"] = np.array([1, 0.0, 0.0, pen.gamma, lam, params.curvature, iters])
+
+    # --- smooth_color (smoother.py:175-217)
+    rgb = np.random.default_rng(6).random((16, 14, 3))
+    img = ref.MultiImage.from_array(rgb)
+    params = ref.SmoothParams(ref.Charbonnier(0.8, 1e-4), 1.0)
+    out, tr = ref.smooth_color(img, params, trace=True)
+    g["sc_rgb_in"] = rgb
+    g["sc_rgb_out"] = out.to_array()
+    g["sc_rgb_energies"] = np.array(tr.energies)
+    lum = replace(params, color_mode=ref.ColorMode.LUMINANCE_ONLY)
+    out_l = ref.smooth_color(img, lum)
+    g["sc_lum_out"] = out_l.to_array()
+
+    # --- C1 oracle config: 512x512 uniform rng(0), N=4, p=0.8.
+    # Stored as a checksum set, not the full plane.
+    f = np.random.default_rng(0).random((512, 512))
+    u = ref.smooth_plane(f, ref.SmoothParams(ref.Charbonnier(0.8, 1e-4), 1.0, iters=4))
+    g["c1_sum"] = np.array([u.sum(), (u * u).sum(), u.min(), u.max()])
+    g["c1_rows"] = u[[0, 1, 255, 511], :]  # four full rows for pointwise checks
+    g["c1_cols"] = u[:, [0, 7, 300, 511]]
+
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
