@@ -1,0 +1,334 @@
+"""Benchmark: 1080p colour ILS frames/s (N=4) on B200, plus HBM roofline fraction.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Workload (BASELINE.json configs[2], the metric's config): 1920x1080 RGB
+frames, Charbonnier p=0.8, eps=1e-4, lambda=1, 4 iterations, c = c0.  A
+"step" smooths a batch of F frames per GPU (synthetic uniform [0,1) planes,
+rng.random as in the reference bench cli.py:270-273, generated on device).
+F frames x 24.9 MB > L2, so each step's inputs stream from HBM; within a
+frame group the working set (f + two half spectra, ~75 MB) stays in L2 across
+the iterations, by design.  Frames shard across ranks with no communication
+(scaling "weak").
+
+value     device throughput: frames/s over all ranks, inputs resident in HBM,
+          one CUDA-graph replay per step, CUDA events, max over ranks.
+e2e       the same through the C ABI with HOST buffers (ils_smooth_host):
+          pinned host -> device copies, kernels, device -> host copies and the
+          status readback inside the timed region, pipelined over frames.
+roofline  the dominant kernel (fused row pass, iterations >= 1) timed alone
+          with CUDA events on its stream: algorithmic bytes / time vs the
+          measured HBM copy bandwidth in MEASURED_PEAKS.json.
+cpu_baseline  the oracle port (numpy/scipy, the reference's own algorithm)
+          on the host cores, one frame.
+--impl reference  times that CPU path alone, as the driver's reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W, CH, ITERS = 1080, 1920, 3, 4
+P_EXP, EPS, LAM = 0.8, 1e-4, 1.0
+METRIC = "1080p colour ILS frames/s (4 iters) on 1/2/4/8 B200; HBM roofline fraction"
+
+
+def bytes_per_frame(iters=ITERS, h=H, w=W, ch=CH):
+    """Algorithmic HBM bytes per frame: (20 N + 4) H W per plane (fp32)."""
+    wc = w // 2 + 1
+    spec = h * wc * 8
+    plane = h * w * 4
+    per_plane = (plane + spec) + iters * 2 * spec + (iters - 1) * (2 * spec + plane) + (spec + plane)
+    return ch * per_plane
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        smax = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_port_frame_seconds(frames=1, seed=20240607):
+    """Oracle port (the reference algorithm, numpy + scipy.fft) on one 1080p RGB frame."""
+    from oracle import ils_oracle as O
+
+    workers = os.cpu_count() or 1
+    planes = O.bench_planes(H, W, CH, seed=seed)
+    pen = O.Charbonnier(P_EXP, EPS)
+    O.smooth_color(planes[:1], pen, LAM, ITERS, workers=workers)  # warm-up (plans, pages)
+    t0 = time.perf_counter()
+    for _ in range(frames):
+        O.smooth_color(planes, pen, LAM, ITERS, workers=workers)
+    return (time.perf_counter() - t0) / frames, workers
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference's algorithm on host cores (oracle port)."""
+    if rank != 0:
+        return
+    sec, workers = cpu_port_frame_seconds(frames=1)  # warm-up + one sample
+    samples = []
+    for _ in range(max(1, args.steps)):
+        s, _ = cpu_port_frame_seconds(frames=1)
+        samples.append(s)
+    mean = sum(samples) / len(samples)
+    fps = 1.0 / mean
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": len(samples), "warmup": 1, "ms_per_step": round(mean * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
+                   "frames_per_step": 1, "impl": "oracle port of ilsmooth.smooth_color (numpy/scipy.fft)"},
+        "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": workers, "kind": "port",
+                         "sample": "1 frame (3 planes 1920x1080) per step, scipy.fft workers=cpu_count"},
+        "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--frames", type=int, default=16, help="frames per step per GPU")
+    ap.add_argument("--group", type=int, default=1, help="frames per ils_smooth call (L2-resident group)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    F = args.frames
+    G = max(1, min(args.group, F))
+    assert F % G == 0, "--frames must be a multiple of --group"
+    params = ils.SmoothParams(ils.Charbonnier(P_EXP, EPS), LAM, iters=ITERS)
+    cp = params.c_params()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(20240607 + rank)
+    f = torch.rand((F * CH, H, W), generator=gen, device=dev, dtype=torch.float32)
+    u = torch.empty_like(f)
+    plan = rt.get_plan(G * CH, H, W, cp, _lib.ILS_F32, local)
+    L = _lib.lib()
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    ps = H * W
+
+    def step_launches(s):
+        for g0 in range(0, F, G):
+            off = g0 * CH * ps * 4
+            _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f.data_ptr() + off), C.c_void_p(u.data_ptr() + off), ps,
+                                    C.c_void_p(ws.data_ptr()), C.c_void_p(s.cuda_stream),
+                                    C.c_void_p(status.data_ptr()), None), "ils_smooth")
+
+    # ---- device throughput: one CUDA graph per step
+    with torch.cuda.stream(stream):
+        step_launches(stream)  # warm the plans / attributes outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step_launches(stream)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    rt.raise_status(int(status.item()))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            e1.record(stream)
+        barrier()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    rt.raise_status(int(status.item()))
+    value = world * F / (ms_step / 1e3)
+    launches = args.steps * (F // G) * plan.info["launches_per_call"]
+
+    # ---- dominant kernel alone (fused row pass, iteration >= 1) and the column pass
+    def time_pass(pass_id, reps=20):
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                L.ils_launch_pass(plan.ptr, pass_id, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()), ps,
+                                  C.c_void_p(ws.data_ptr()), C.c_void_p(stream.cuda_stream),
+                                  C.c_void_p(status.data_ptr()))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                _lib.check(L.ils_launch_pass(plan.ptr, pass_id, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()),
+                                             ps, C.c_void_p(ws.data_ptr()), C.c_void_p(stream.cuda_stream),
+                                             C.c_void_p(status.data_ptr())), "ils_launch_pass")
+            b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    ms_row = time_pass(2)
+    ms_col = time_pass(1)
+    wc = W // 2 + 1
+    planes_g = G * CH
+    row_bytes = planes_g * (2 * H * wc * 8 + H * W * 4)
+    col_bytes = planes_g * (2 * H * wc * 8)
+    peak, peak_kind = peaks()
+    row_gbs = row_bytes / (ms_row / 1e3) / 1e9
+    col_gbs = col_bytes / (ms_col / 1e3) / 1e9
+
+    # ---- end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        fh = torch.empty((F * CH, H, W), dtype=torch.float32, pin_memory=True)
+        fh.copy_(f.cpu())
+        uh = torch.empty_like(fh, pin_memory=True)
+        io = C.c_size_t()
+        _lib.check(L.ils_host_io_size(plan.ptr, C.byref(io)), "ils_host_io_size")
+        iobuf = torch.empty(io.value, dtype=torch.uint8, device=dev)
+        bad = C.c_int32()
+
+        def host_call():
+            _lib.check(L.ils_smooth_host(plan.ptr, C.c_void_p(fh.data_ptr()), C.c_void_p(uh.data_ptr()), ps, F // G,
+                                         C.c_void_p(ws.data_ptr()), C.c_void_p(iobuf.data_ptr()),
+                                         C.c_void_p(stream.cuda_stream), C.byref(bad)), "ils_smooth_host")
+
+        for _ in range(max(1, args.warmup)):
+            host_call()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_steps = max(1, args.steps // 2)
+        a.record(stream)
+        for _ in range(e2e_steps):
+            host_call()
+        b.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(a.elapsed_time(b) / e2e_steps)
+        assert torch.equal(uh[:CH].to(dev), u[:CH]), "e2e output differs from device path"
+        e2e = {"value": round(world * F / (ms_e2e / 1e3), 2), "unit": "frames/s",
+               "h2d_bytes_per_step": F * CH * H * W * 4, "d2h_bytes_per_step": F * CH * H * W * 4 + (F // G) * 4,
+               "ms_per_step": round(ms_e2e, 3), "api": "ils_smooth_host (C ABI), pinned host fp32 planes"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sec, workers = cpu_port_frame_seconds(frames=1)
+        cpu = {"value": round(1.0 / sec, 4), "unit": "frames/s", "cores": workers, "kind": "port",
+               "sample": "1 frame (3 planes 1920x1080), oracle port of smooth_color, scipy.fft workers=cpu_count"}
+
+    if rank == 0:
+        bpf = bytes_per_frame()
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
+                       "frames_per_step_per_gpu": F, "frames_per_launch_group": G,
+                       "parallelism": f"frame-sharded x{world}", "l2": "inputs larger than L2 (F x 24.9 MB)",
+                       "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec",
+                                                          "col_cols", "col_group", "col_radix", "col_spec")}},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": round(row_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(row_gbs / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "k_row fused row pass (iteration>=1)", "ms": round(ms_row, 4),
+                         "bytes_per_launch": row_bytes,
+                         "col_pass": {"achieved": round(col_gbs, 1), "frac": round(col_gbs / peak, 4),
+                                      "ms": round(ms_col, 4), "bytes_per_launch": col_bytes},
+                         "whole_path": {"achieved": round(bpf * value / world / 1e9, 1),
+                                        "frac": round(bpf * value / world / 1e9 / peak, 4),
+                                        "bytes_per_frame": bpf}},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

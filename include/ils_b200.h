@@ -1,0 +1,149 @@
+/*
+ * ils_b200.h -- C ABI of the B200-native ILS smoothing hot path.
+ *
+ * The reference (ilsmooth, pure Python) has no native ABI; its seam is the
+ * Python API (pkg/src/ilsmooth/__init__.py:44-61) plus the FFT seam
+ * solver._fft2/_ifft2 (solver.py:24-30).  Each entry point below states the
+ * reference interface it replaces.  All functions are plain C: pointers,
+ * sizes, POD structs; no torch types.  Device pointers are CUDA global memory
+ * on the plan's device; `stream` is a cudaStream_t passed as void*.
+ *
+ * Errors are status codes here and exceptions in the Python layer:
+ *   ILS_EINVAL, ILS_ENONFINITE_INPUT, ILS_EUNSUPPORTED -> ValueError
+ *   ILS_ENONFINITE                                     -> NumericalError
+ * (errors.py:10-15; raise sites image.py:43-44, smoother.py:166-167,
+ *  solver.py:119-125).  ils_last_error() returns a thread-local message.
+ */
+#ifndef ILS_B200_H
+#define ILS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ILS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ILS_API __attribute__((visibility("default")))
+#else
+#define ILS_API
+#endif
+
+typedef enum {
+  ILS_OK = 0,
+  ILS_EINVAL = 1,           /* bad parameters / shapes / plan mismatch -> ValueError */
+  ILS_ENONFINITE_INPUT = 2, /* non-finite input plane -> ValueError (image.py:43-44) */
+  ILS_ENONFINITE = 3,       /* non-finite iterate -> NumericalError (smoother.py:166-167) */
+  ILS_ECUDA = 4,            /* CUDA runtime failure */
+  ILS_EUNSUPPORTED = 5      /* a side has a prime factor > 61 -> ValueError */
+} ils_status;
+
+typedef enum { ILS_CHARBONNIER = 0, ILS_WELSCH = 1 } ils_penalty_kind;
+typedef enum { ILS_F32 = 0, ILS_F64 = 1 } ils_dtype;
+
+/* Value of a device status word that saw no failure (memset pattern 0x7f). */
+#define ILS_STATUS_CLEAN 0x7f7f7f7f
+
+/* SmoothParams (smoother.py:31-62) + penalty (penalty.py:47-105), flattened.
+ * c must already be resolved (SmoothParams.curvature, smoother.py:60-62). */
+typedef struct {
+  int32_t kind;  /* ils_penalty_kind */
+  double p;      /* Charbonnier exponent, (0, 1]       (penalty.py:54-56) */
+  double eps;    /* Charbonnier eps > 0                  (penalty.py:57-58) */
+  double gamma;  /* Welsch gamma > 0                     (penalty.py:84-86) */
+  double lam;    /* lambda > 0, finite                   (smoother.py:47-48) */
+  double c;      /* curvature >= min_curvature(1-1e-12) (smoother.py:51-56) */
+  int32_t iters; /* >= 1                                 (smoother.py:49-50) */
+} ils_params;
+
+typedef struct ils_plan ils_plan;
+
+/* make_plan(height, width, lam, c) (solver.py:78-106) for a batch of `batch`
+ * planes of height x width, computing in `dtype` on CUDA `device`.  Holds the
+ * FFT radix plans, twiddle tables and the 1-D spectral-denominator tables.
+ * Immutable after creation; safe to share across threads and streams. */
+ILS_API ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_t width, const ils_params* params,
+                           int32_t dtype, int32_t device);
+ILS_API void ils_plan_destroy(ils_plan* plan);
+
+/* Bytes of device workspace one in-flight ils_smooth/ils_solve_ls call needs
+ * (two half spectra + trace partials).  One workspace per concurrent call. */
+ILS_API ils_status ils_workspace_size(const ils_plan* plan, size_t* bytes);
+
+/* smooth_plane / smooth_color(PER_CHANNEL_RGB) (smoother.py:132-217): all
+ * params.iters ILS iterations on `batch` planes.  f_dev/u_dev: planar
+ * [batch][height][width] with rows contiguous and `plane_stride` elements
+ * between planes.  status_dev (int32, device): set to ILS_STATUS_CLEAN, then
+ * atomically lowered to the first non-finite iteration (0 = input).
+ * energies_dev (double, device, optional): (iters+1) x batch energies,
+ * iteration-major (smoother.py:93-101, 161, 168-169).  Asynchronous. */
+ILS_API ils_status ils_smooth(const ils_plan* plan, const void* f_dev, void* u_dev, int64_t plane_stride, void* workspace,
+                      void* stream, int32_t* status_dev, double* energies_dev);
+
+/* Same, with HOST buffers: `nbatches` consecutive batches of plan.batch
+ * planes (plane_stride elements apart) are copied in, smoothed and copied
+ * out, pipelined so batch k+1's host->device copy and batch k-1's
+ * device->host copy overlap batch k's kernels (two I/O slots, three
+ * streams).  Blocks until done, then decodes the status words: returns
+ * ILS_ENONFINITE_INPUT / ILS_ENONFINITE with *bad_iter = first bad iteration
+ * (-1 when clean).  workspace: ils_workspace_size bytes; io_dev:
+ * ils_host_io_size bytes of device memory.  Host buffers should be pinned
+ * (cudaHostAlloc) for the copies to overlap. */
+ILS_API ils_status ils_host_io_size(const ils_plan* plan, size_t* bytes);
+ILS_API ils_status ils_smooth_host(const ils_plan* plan, const void* f_host, void* u_host, int64_t plane_stride,
+                                   int32_t nbatches, void* workspace, void* io_dev, void* stream, int32_t* bad_iter);
+
+/* One pass of the ils_smooth launch sequence on its own (roofline timing and
+ * profiling): pass 0 = row pass from f (iteration 0), 1 = column solve pass,
+ * 2 = fused row pass (iteration >= 1), 3 = final row pass writing u.  Uses
+ * the workspace's first half spectrum as input and output. */
+ILS_API ils_status ils_launch_pass(const ils_plan* plan, int32_t pass, const void* f_dev, void* u_dev,
+                                   int64_t plane_stride, void* workspace, void* stream, int32_t* status_dev);
+
+/* solve_ls(plan, f, mu_x, mu_y) (solver.py:109-134): one least-squares
+ * solve per plane.  status_dev is lowered to 1/2/3 when f/mu_x/mu_y hold a
+ * non-finite value (solver.py:119-125). */
+ILS_API ils_status ils_solve_ls(const ils_plan* plan, const void* f_dev, const void* mu_x_dev, const void* mu_y_dev,
+                        void* u_dev, int64_t plane_stride, void* workspace, void* stream, int32_t* status_dev);
+
+/* The hand-written real 2-D transforms on their own (the FFT seam
+ * solver._fft2/_ifft2, restricted to real data): rfft2 writes the half
+ * spectrum [batch][height][width/2+1] (complex, interleaved) with row pitch
+ * `spec_pitch` complex elements; irfft2 is its normalised inverse.
+ * irfft2 destroys its input spectrum. */
+ILS_API ils_status ils_rfft2(const ils_plan* plan, const void* x_dev, int64_t plane_stride, void* spec_dev, int64_t spec_pitch,
+                     void* stream);
+ILS_API ils_status ils_irfft2(const ils_plan* plan, void* spec_dev, int64_t spec_pitch, void* x_dev, int64_t plane_stride,
+                      void* stream);
+
+/* BT.601 conversion of [frames][3][plane] in place (image.py:110-128);
+ * used by ColorMode.LUMINANCE_ONLY (smoother.py:195-202). */
+ILS_API ils_status ils_rgb_yuv(void* planes_dev, int32_t dtype, int64_t plane_stride, int64_t npx, int32_t frames,
+                       int32_t inverse, void* stream);
+
+/* Introspection for tests and the bench. */
+typedef struct {
+  int32_t batch, height, width, dtype, packed;
+  int32_t row_band, row_threads, row_grid, row_smem;
+  int32_t col_cols, col_threads, col_grid, col_smem;
+  int32_t row_passes, col_passes;
+  int32_t row_group, col_group; /* threads per FFT line group */
+  int32_t row_spec, col_spec;   /* compile-time FFT plan id, -1 = runtime plan */
+  int32_t row_radix[16];
+  int32_t col_radix[16];
+  int64_t spec_pitch;        /* complex elements per spectrum row */
+  int32_t launches_per_call; /* kernels one ils_smooth launches (no trace) */
+} ils_plan_info;
+ILS_API ils_status ils_plan_get_info(const ils_plan* plan, ils_plan_info* info);
+
+ILS_API const char* ils_last_error(void);
+ILS_API int32_t ils_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ILS_B200_H */

@@ -1,0 +1,24 @@
+"""B200-native ILS edge-preserving smoothing (drop-in for ilsmooth's smoothing path).
+
+Public API mirrors the reference package's hot path (pkg/src/ilsmooth/
+__init__.py:44-61): SmoothParams, Charbonnier, Welsch, ColorMode, MultiImage,
+smooth_plane, smooth_color, make_plan, solve_ls, SolverPlan, EnergyTrace and
+the error types.  Every arithmetic step runs in libils_b200.so (hand-written
+sm_100a CUDA) behind the C ABI in include/ils_b200.h; there is no CPU path.
+"""
+
+from ._runtime import get_default_precision, set_default_precision
+from .errors import ImageFormatError, NumericalError
+from .image import GRAY, RGB, YUV, ColorMode, MultiImage, as_plane, rgb_to_yuv, yuv_to_rgb
+from .penalty import DEFAULT_EPS, Charbonnier, Welsch, check_curvature
+from .smoother import EnergyTrace, SmoothParams, smooth_batch, smooth_color, smooth_plane
+from .solver import SolverPlan, make_plan, solve_ls
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DEFAULT_EPS", "GRAY", "RGB", "YUV", "Charbonnier", "ColorMode", "EnergyTrace", "ImageFormatError",
+    "MultiImage", "NumericalError", "SmoothParams", "SolverPlan", "Welsch", "as_plane", "check_curvature",
+    "get_default_precision", "make_plan", "rgb_to_yuv", "set_default_precision", "smooth_batch", "smooth_color",
+    "smooth_plane", "solve_ls", "yuv_to_rgb",
+]

@@ -1,0 +1,221 @@
+"""Device plumbing: plan cache, workspaces, host<->device moves (torch).
+
+torch provides device memory, streams and the caching allocator; every
+arithmetic step of the smoothing path is a kernel in libils_b200.so called
+through the C ABI (_lib.py).  Nothing here computes on the CPU, and nothing
+falls back: without CUDA the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _lib
+from .errors import NumericalError
+
+_PRECISION = os.environ.get("ILS_PRECISION", "fp32")
+_plans: "OrderedDict[tuple, DevicePlan]" = OrderedDict()
+_plans_lock = threading.Lock()
+_MAX_PLANS = 32
+
+
+def set_default_precision(p: str) -> None:
+    """'fp32' (default, the throughput path) or 'fp64' (tight parity)."""
+    global _PRECISION
+    if p not in ("fp32", "fp64"):
+        raise ValueError(f"precision must be 'fp32' or 'fp64', got {p!r}")
+    _PRECISION = p
+
+
+def get_default_precision() -> str:
+    return _PRECISION
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2003_07504_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch
+
+
+def torch_dtype(precision):
+    torch = _torch()
+    precision = precision or _PRECISION
+    if precision == "fp32":
+        return torch.float32
+    if precision == "fp64":
+        return torch.float64
+    raise ValueError(f"precision must be 'fp32' or 'fp64', got {precision!r}")
+
+
+class DevicePlan:
+    """Owns one ils_plan* (make_plan analogue, solver.py:78-106)."""
+
+    def __init__(self, batch, height, width, cparams, dtype_code, device_index):
+        L = _lib.lib()
+        h = C.c_void_p()
+        _lib.check(L.ils_plan_create(C.byref(h), batch, height, width, C.byref(cparams), dtype_code, device_index),
+                   "ils_plan_create")
+        self.ptr = h
+        self.batch, self.height, self.width = batch, height, width
+        self.dtype_code = dtype_code
+        self.iters = cparams.iters
+        ws = C.c_size_t()
+        _lib.check(L.ils_workspace_size(h, C.byref(ws)), "ils_workspace_size")
+        self.workspace_bytes = ws.value
+        info = _lib.PlanInfo()
+        _lib.check(L.ils_plan_get_info(h, C.byref(info)), "ils_plan_get_info")
+        self.info = info.as_dict()
+
+    def __del__(self):
+        try:
+            if getattr(self, "ptr", None):
+                _lib.lib().ils_plan_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+def get_plan(batch, height, width, cparams, dtype_code, device_index) -> DevicePlan:
+    key = (batch, height, width, cparams.kind, cparams.p, cparams.eps, cparams.gamma, cparams.lam, cparams.c,
+           cparams.iters, dtype_code, device_index)
+    with _plans_lock:
+        plan = _plans.get(key)
+        if plan is None:
+            plan = DevicePlan(batch, height, width, cparams, dtype_code, device_index)
+            _plans[key] = plan
+            while len(_plans) > _MAX_PLANS:
+                _plans.popitem(last=False)
+        else:
+            _plans.move_to_end(key)
+        return plan
+
+
+def _stream_ptr(torch, device):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def smooth_device(f, cparams, trace=False, check=True):
+    """All ILS iterations on a CUDA tensor f[B, H, W] (one launch sequence).
+
+    Returns (u, energies[(iters+1), B] or None, status tensor).  With
+    check=True the status word is read back and mapped to the reference's
+    exceptions (ValueError for a non-finite input plane, NumericalError for
+    a non-finite iterate, smoother.py:166-167).
+    """
+    torch = _torch()
+    if f.dim() != 3 or not f.is_cuda:
+        raise ValueError("smooth_device expects a CUDA tensor [B, H, W]")
+    f = f.contiguous()
+    B, H, W = f.shape
+    code = _lib.ILS_F32 if f.dtype == torch.float32 else _lib.ILS_F64
+    if f.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"unsupported dtype {f.dtype}")
+    dev = f.device
+    plan = get_plan(B, H, W, cparams, code, dev.index if dev.index is not None else torch.cuda.current_device())
+    u = torch.empty_like(f)
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    energies = torch.empty((cparams.iters + 1, B), dtype=torch.float64, device=dev) if trace else None
+    L = _lib.lib()
+    _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()), H * W,
+                            C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev), C.c_void_p(status.data_ptr()),
+                            C.c_void_p(energies.data_ptr()) if trace else None), "ils_smooth")
+    if check:
+        raise_status(int(status.item()))
+    return u, energies, status
+
+
+def raise_status(s: int) -> None:
+    if s == _lib.STATUS_CLEAN:
+        return
+    if s == 0:
+        raise ValueError("image plane contains non-finite values")
+    raise NumericalError(f"non-finite iterate at iteration {s}")
+
+
+def solve_device(f, mx, my, cparams):
+    """solve_ls on CUDA tensors [B, H, W] (solver.py:109-134)."""
+    torch = _torch()
+    f, mx, my = (t.contiguous() for t in (f, mx, my))
+    B, H, W = f.shape
+    code = _lib.ILS_F32 if f.dtype == torch.float32 else _lib.ILS_F64
+    dev = f.device
+    plan = get_plan(B, H, W, cparams, code, dev.index if dev.index is not None else torch.cuda.current_device())
+    u = torch.empty_like(f)
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    L = _lib.lib()
+    _lib.check(L.ils_solve_ls(plan.ptr, C.c_void_p(f.data_ptr()), C.c_void_p(mx.data_ptr()),
+                              C.c_void_p(my.data_ptr()), C.c_void_p(u.data_ptr()), H * W,
+                              C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev), C.c_void_p(status.data_ptr())),
+               "ils_solve_ls")
+    s = int(status.item())
+    if s != _lib.STATUS_CLEAN:
+        raise NumericalError(f"non-finite values in {('f', 'mu_x', 'mu_y')[s - 1]}")
+    return u
+
+
+def rfft2_device(x, cparams=None):
+    """Hand-written real 2-D FFT of x[B, H, W] -> complex [B, H, W//2+1]."""
+    torch = _torch()
+    x = x.contiguous()
+    B, H, W = x.shape
+    code = _lib.ILS_F32 if x.dtype == torch.float32 else _lib.ILS_F64
+    cparams = cparams or _dummy_params()
+    plan = get_plan(B, H, W, cparams, code, x.device.index or 0)
+    pitch = plan.info["spec_pitch"]
+    cdt = torch.complex64 if code == _lib.ILS_F32 else torch.complex128
+    spec = torch.empty((B, H, pitch), dtype=cdt, device=x.device)
+    _lib.check(_lib.lib().ils_rfft2(plan.ptr, C.c_void_p(x.data_ptr()), H * W, C.c_void_p(spec.data_ptr()), pitch,
+                                    _stream_ptr(torch, x.device)), "ils_rfft2")
+    return spec[:, :, : W // 2 + 1]
+
+
+def irfft2_device(spec, width, cparams=None):
+    """Inverse of rfft2_device (normalised like numpy.fft.irfft2)."""
+    torch = _torch()
+    B, H, Wc = spec.shape
+    code = _lib.ILS_F32 if spec.dtype == torch.complex64 else _lib.ILS_F64
+    cparams = cparams or _dummy_params()
+    plan = get_plan(B, H, width, cparams, code, spec.device.index or 0)
+    pitch = plan.info["spec_pitch"]
+    buf = torch.zeros((B, H, pitch), dtype=spec.dtype, device=spec.device)
+    buf[:, :, :Wc] = spec
+    rdt = torch.float32 if code == _lib.ILS_F32 else torch.float64
+    x = torch.empty((B, H, width), dtype=rdt, device=spec.device)
+    _lib.check(_lib.lib().ils_irfft2(plan.ptr, C.c_void_p(buf.data_ptr()), pitch, C.c_void_p(x.data_ptr()),
+                                     H * width, _stream_ptr(torch, spec.device)), "ils_irfft2")
+    return x
+
+
+def _dummy_params():
+    return _lib.Params(_lib.ILS_WELSCH, 0.0, 0.0, 1.0, 1.0, 2.0, 1)
+
+
+def rgb_yuv_(planes, inverse: bool) -> None:
+    """In-place BT.601 conversion of CUDA planes [F*3, H, W] (image.py:110-128)."""
+    torch = _torch()
+    n3, H, W = planes.shape
+    code = _lib.ILS_F32 if planes.dtype == torch.float32 else _lib.ILS_F64
+    _lib.check(_lib.lib().ils_rgb_yuv(C.c_void_p(planes.data_ptr()), code, H * W, H * W, n3 // 3, int(inverse),
+                                      _stream_ptr(torch, planes.device)), "ils_rgb_yuv")
+
+
+def to_device_planes(planes, precision=None):
+    """Stack host planes into one CUDA tensor [B, H, W] of the target dtype."""
+    torch = _torch()
+    dt = torch_dtype(precision)
+    host = np.stack([np.asarray(p, dtype=np.float64) for p in planes])
+    return torch.from_numpy(host).to("cuda").to(dt)  # f64 over PCIe, narrowed on the device
+
+
+def to_host_f64(t):
+    arr = t.detach().to("cpu").to(dtype=_torch().float64).numpy()
+    return [np.ascontiguousarray(arr[i]) for i in range(arr.shape[0])]

@@ -1,0 +1,801 @@
+// C ABI of the ILS hot path: plans, launch sequencing, host I/O pipeline.
+//
+// Reference interfaces replaced (see include/ils_b200.h for the per-function
+// citations): make_plan/SolverPlan (solver.py:52-106), solve_ls
+// (solver.py:109-134), smooth_plane/smooth_color (smoother.py:132-217).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ils_b200.h"
+#include "ils_kernels.cuh"
+
+using namespace ils;
+
+namespace {
+
+thread_local std::string g_err;
+
+ils_status fail(ils_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define ILS_CUDA(call)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess) return fail(ILS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));     \
+  } while (0)
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+// ------------------------------------------------------------ radix planning
+const int kUnrolled[] = {16, 15, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2};
+
+// A group of G threads owns one n-point line; a radix-R pass gives each
+// thread ceil((n/R)/G) butterflies, which must fit its KM = MAXE/R slots
+// (generic primes: one butterfly per thread).
+bool pass_fits(int R, long long n, int G, int maxe) {
+  const long long tasks = n / R;
+  const int km = (R <= 16) ? std::max(1, maxe / R) : 1;
+  return (tasks + G - 1) / G <= km;
+}
+
+struct FftHost {
+  int n = 1;
+  int G = 32;
+  std::vector<int> radix;
+  std::vector<int> tw_off, gen_off;
+  std::vector<double> tw;  // interleaved re/im
+};
+
+bool better(const std::vector<int>& a, const std::vector<int>& b) {
+  if (b.empty()) return true;
+  if (a.size() != b.size()) return a.size() < b.size();
+  const int ma = *std::min_element(a.begin(), a.end()), mb = *std::min_element(b.begin(), b.end());
+  if (ma != mb) return ma > mb;
+  return a > b;
+}
+
+void dfs(int rem, int maxr, long long elems, int nthr, int maxe, std::vector<int>& cur, std::vector<int>& best,
+         bool& found) {
+  if (rem == 1) {
+    if (!found || better(cur, best)) best = cur;
+    found = true;
+    return;
+  }
+  if (found && cur.size() + 1 > best.size()) return;
+  // generic odd primes 17..61 must stand alone
+  for (int p = 17; p <= kMaxGenericPrime; p += 2) {
+    bool prime = true;
+    for (int d = 3; d * d <= p; d += 2)
+      if (p % d == 0) prime = false;
+    if (prime && rem % p == 0) {
+      if (p > maxr || !pass_fits(p, elems, nthr, maxe)) return;
+      cur.push_back(p);
+      dfs(rem / p, p, elems, nthr, maxe, cur, best, found);
+      cur.pop_back();
+      return;
+    }
+  }
+  for (int R : kUnrolled) {
+    if (R > maxr || rem % R) continue;
+    if (!pass_fits(R, elems, nthr, maxe)) continue;
+    cur.push_back(R);
+    dfs(rem / R, R, elems, nthr, maxe, cur, best, found);
+    cur.pop_back();
+  }
+}
+
+bool has_big_prime(int n) {
+  for (int p = 2; (long long)p * p <= n; ++p)
+    while (n % p == 0) n /= p;
+  return n > kMaxGenericPrime;
+}
+
+struct SpecHost {
+  int id, n;
+  std::vector<int> radix;
+};
+#define ILS_HOST_SPEC(ID, N, ...) SpecHost{ID, N, {__VA_ARGS__}},
+const SpecHost kRowSpecs[] = {ILS_ROW_SPECS(ILS_HOST_SPEC)};
+const SpecHost kColSpecs[] = {ILS_COL_SPECS(ILS_HOST_SPEC)};
+#undef ILS_HOST_SPEC
+
+// Radix plan + twiddles for an n-point line transform.  A compile-time spec
+// (fp32 hot sizes) fixes the radices; otherwise the plan with fewest passes.
+// G is the smallest group size (32..256) for which every pass fits.
+bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec) {
+  out = FftHost{};
+  out.n = n;
+  bool ok = n <= 1;
+  for (int G = 32; G <= 256 && !ok; G *= 2) {
+    if (spec) {
+      bool fits = true;
+      for (int R : spec->radix) fits = fits && pass_fits(R, n, G, maxe);
+      if (fits) {
+        out.radix = spec->radix;
+        out.G = G;
+        ok = true;
+      }
+      continue;
+    }
+    std::vector<int> cur, best;
+    bool found = false;
+    dfs(n, 1 << 30, n, G, maxe, cur, best, found);
+    if (found) {
+      out.radix = best;
+      out.G = G;
+      ok = true;
+    }
+  }
+  if (!ok) return false;
+  if ((int)out.radix.size() > kMaxPass) return false;
+  long long Ns = 1;
+  for (int R : out.radix) {
+    out.tw_off.push_back((int)(out.tw.size() / 2));
+    for (long long m = 0; m < Ns; ++m)
+      for (int r = 1; r < R; ++r) {
+        const sc_t w = sincos2pi(-(long long)r * m, Ns * R);
+        out.tw.push_back(w.c);
+        out.tw.push_back(w.s);
+      }
+    out.gen_off.push_back((int)(out.tw.size() / 2));
+    if (R > 16)
+      for (int q = 0; q < R; ++q) {
+        const sc_t w = sincos2pi(-q, R);
+        out.tw.push_back(w.c);
+        out.tw.push_back(w.s);
+      }
+    Ns *= R;
+  }
+  return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ plan
+struct ils_plan {
+  int B, H, W, N, Wc, Sp;
+  bool packed;
+  int dtype, device;
+  ils_params prm;
+  int band, row_threads, row_grid, LP;
+  size_t row_smem;
+  int C, CS, col_threads, col_grid;
+  size_t col_smem;
+  int row_spec = -1, col_spec = -1;  // compile-time FFT plan ids (-1: runtime plan)
+  FftHost rowf, colf;
+  void* d_tables = nullptr;
+  size_t off_rowtw, off_coltw, off_wreal, off_wx, off_wy, off_sink;  // byte offsets
+  size_t spec_bytes;                                       // one half spectrum
+  size_t epart_elems;                                      // doubles for trace partials
+};
+
+namespace {
+
+template <typename T>
+size_t esz() {
+  return sizeof(cx<T>);
+}
+
+int padded_len_rt(int n, size_t elt) {
+  return elt == 8 ? padded_len<float>(n) : padded_len<double>(n);
+}
+
+template <size_t K>
+const SpecHost* find_spec(const SpecHost (&tab)[K], int n) {
+  if (env_int("ILS_NO_SPECS", 0)) return nullptr;
+  for (const SpecHost& s : tab)
+    if (s.n == n) return &s;
+  return nullptr;
+}
+
+bool choose_row(ils_plan& p, int maxe, size_t elt) {
+  const SpecHost* spec = (p.dtype == ILS_F32 && p.packed) ? find_spec(kRowSpecs, p.N) : nullptr;
+  p.row_spec = spec ? spec->id : -1;
+  if (!make_fft(p.N, maxe, p.rowf, spec)) return false;
+  if (p.W > kWideMaxW || (p.W > kNarrowMaxW && !p.packed)) return false;  // stencil strip registers
+  const int line = p.packed ? p.N + 1 : p.N;
+  const int LP = (padded_len_rt(line, elt) + 1) & ~1;
+  const size_t budget = (size_t)env_int("ILS_SMEM_BUDGET", 110 * 1024);
+  int band = std::min(p.H, env_int("ILS_ROW_BAND", 16));
+  // wide rows: take the whole shared memory rather than a 1-row band
+  const size_t bud = (size_t)LP * elt * 6 > budget ? std::max(budget, (size_t)227 * 1024) : budget;
+  while (band > 1 && (size_t)(band + 2) * LP * elt > bud) --band;
+  if ((size_t)(band + 2) * LP * elt > 227 * 1024) return false;
+  p.band = band;
+  p.row_threads = kRowThreads;
+  p.LP = LP;
+  p.row_smem = (size_t)(band + 2) * LP * elt;
+  p.row_grid = (p.H + band - 1) / band;
+  return true;
+}
+
+bool choose_col(ils_plan& p, int maxe, size_t elt) {
+  const SpecHost* spec = p.dtype == ILS_F32 ? find_spec(kColSpecs, p.H) : nullptr;
+  p.col_spec = spec ? spec->id : -1;
+  if (!make_fft(p.H, maxe, p.colf, spec)) return false;
+  const size_t budget = (size_t)env_int("ILS_SMEM_BUDGET", 110 * 1024);
+  const int E = elt == 8 ? 16 : 8;  // complex elements per 128 B
+  const int fc = env_int("ILS_COL_COLS", 0);
+  const int opts[] = {8, 4, 16, 2, 1};
+  for (int C : opts) {
+    if (fc) C = fc;
+    const int Cu = std::min(C, p.Wc);
+    const int base = (padded_len_rt(p.H, elt) + E - 1) / E * E;
+    const int CS = base + ((32 / std::max(Cu, 1)) % E);
+    const size_t smem = (size_t)Cu * CS * elt;
+    if (smem <= budget || C == 1 || fc) {
+      if (smem > 227 * 1024) return false;
+      p.C = Cu;
+      p.CS = CS;
+      p.col_threads = kColThreads;
+      p.col_smem = smem;
+      p.col_grid = (p.Wc + Cu - 1) / Cu;
+      return true;
+    }
+  }
+  return false;
+}
+
+template <typename T>
+void fill_fft_dev(FftDev<T>& d, const FftHost& h, const void* base, size_t off) {
+  d.n = h.n;
+  d.G = h.G;
+  d.npass = (int)h.radix.size();
+  for (int i = 0; i < kMaxPass; ++i) {
+    d.radix[i] = i < d.npass ? h.radix[i] : 1;
+    d.tw_off[i] = i < d.npass ? h.tw_off[i] : 0;
+    d.gen_off[i] = i < d.npass ? h.gen_off[i] : 0;
+  }
+  d.tw = reinterpret_cast<const cx<T>*>(static_cast<const char*>(base) + off);
+}
+
+template <typename T>
+PenaltyDev<T> pen_dev(const ils_params& q) {
+  PenaltyDev<T> P{};
+  P.kind = q.kind;
+  P.p = T(q.p);
+  P.pe = T(q.p / 2.0 - 1.0);
+  P.ph = T(q.p / 2.0);
+  P.eps = T(q.eps);
+  const double g2 = q.gamma * q.gamma;
+  P.wk = q.kind == ILS_WELSCH ? T(-1.0 / (2.0 * g2)) : T(0);
+  P.g2x2 = T(2.0 * g2);
+  P.c = T(q.c);
+  P.lam = T(q.lam);
+  P.lam2 = T(q.lam / 2.0);
+  return P;
+}
+
+template <typename T>
+RowArgs<T> row_args(const ils_plan* p) {
+  RowArgs<T> a{};
+  a.B = p->B;
+  a.H = p->H;
+  a.W = p->W;
+  a.N = p->N;
+  a.Wc = p->Wc;
+  a.band = p->band;
+  a.LP = p->LP;
+  a.S_rp = p->Sp;
+  a.S_ps = (long long)p->H * p->Sp;
+  a.pen = pen_dev<T>(p->prm);
+  fill_fft_dev<T>(a.fft, p->rowf, p->d_tables, p->off_rowtw);
+  a.wreal = reinterpret_cast<const cx<T>*>(static_cast<const char*>(p->d_tables) + p->off_wreal);
+  return a;
+}
+
+template <typename T>
+ColArgs<T> col_args(const ils_plan* p, cx<T>* S, int mode) {
+  ColArgs<T> a{};
+  a.B = p->B;
+  a.H = p->H;
+  a.Wc = p->Wc;
+  a.C = p->C;
+  a.CS = p->CS;
+  a.S = S;
+  a.S_rp = p->Sp;
+  a.S_ps = (long long)p->H * p->Sp;
+  a.wx = reinterpret_cast<const T*>(static_cast<const char*>(p->d_tables) + p->off_wx);
+  a.wy = reinterpret_cast<const T*>(static_cast<const char*>(p->d_tables) + p->off_wy);
+  a.cl2 = T(p->prm.c * p->prm.lam / 2.0);
+  a.inv_hw = T(1.0 / ((double)p->H * (double)p->W));
+  a.mode = mode;
+  fill_fft_dev<T>(a.fft, p->colf, p->d_tables, p->off_coltw);
+  return a;
+}
+
+template <typename T>
+cudaError_t launch_row(const ils_plan* p, int mode, RowArgs<T> a, cudaStream_t s) {
+  a.mode = mode;
+  const dim3 grid(p->row_grid, p->B);
+  if constexpr (std::is_same<T, float>::value) {
+    switch (p->row_spec) {
+#define ILS_CASE(ID, ...) \
+  case ID:                \
+    return launch_row_impl<float, true, RowSpec<ID>::type, ILS_ROW_SPEC_WIDE(ID)>(a, grid, p->row_threads, p->row_smem, s);
+      ILS_ROW_SPECS(ILS_CASE)
+#undef ILS_CASE
+      default:
+        break;
+    }
+  }
+  if (p->W > kNarrowMaxW) return launch_row_impl<T, true, FftRt, true>(a, grid, p->row_threads, p->row_smem, s);
+  return p->packed ? launch_row_impl<T, true, FftRt>(a, grid, p->row_threads, p->row_smem, s)
+                   : launch_row_impl<T, false, FftRt>(a, grid, p->row_threads, p->row_smem, s);
+}
+
+template <typename T>
+cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
+  const dim3 grid(p->col_grid, p->B);
+  if constexpr (std::is_same<T, float>::value) {
+    switch (p->col_spec) {
+#define ILS_CASE(ID, ...) \
+  case ID:                \
+    return launch_col_impl<float, ColSpec<ID>::type>(a, grid, p->col_threads, p->col_smem, s);
+      ILS_COL_SPECS(ILS_CASE)
+#undef ILS_CASE
+      default:
+        break;
+    }
+  }
+  return launch_col_impl<T, FftRt>(a, grid, p->col_threads, p->col_smem, s);
+}
+
+template <typename T>
+ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, cudaStream_t s, int32_t* status,
+                    double* energies) {
+  cx<T>* Sa = static_cast<cx<T>*>(ws);
+  cx<T>* Sb = reinterpret_cast<cx<T>*>(static_cast<char*>(ws) + p->spec_bytes);
+  double* ep = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * p->spec_bytes + 256);
+  const size_t per_pass = (size_t)p->B * p->row_grid;
+  ILS_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t), s));
+  RowArgs<T> a = row_args<T>(p);
+  a.f = f;
+  a.f_ps = ps;
+  a.f_rp = p->W;
+  a.u = u;
+  a.u_ps = ps;
+  a.u_rp = p->W;
+  a.status = status;
+  const int iters = p->prm.iters;
+  cx<T>* cur = Sa;
+  cx<T>* nxt = Sb;
+  for (int n = 0; n < iters; ++n) {
+    a.iter = n;
+    a.Sin = n == 0 ? nullptr : cur;
+    a.Sout = n == 0 ? cur : nxt;
+    a.epart = energies ? ep + n * per_pass : nullptr;
+    ILS_CUDA(launch_row<T>(p, n == 0 ? MODE_F0 : MODE_IT, a, s));
+    if (n > 0) std::swap(cur, nxt);
+    ILS_CUDA(launch_col<T>(p, col_args<T>(p, cur, COL_SOLVE), s));
+  }
+  a.iter = iters;
+  a.Sin = cur;
+  a.Sout = nullptr;
+  a.epart = energies ? ep + iters * per_pass : nullptr;
+  ILS_CUDA(launch_row<T>(p, MODE_FIN, a, s));
+  if (energies) {
+    for (int n = 0; n <= iters; ++n) {
+      k_energy_reduce<<<p->B, 256, 0, s>>>(ep + n * per_pass, p->row_grid, p->B, energies + (size_t)n * p->B);
+    }
+    ILS_CUDA(cudaGetLastError());
+  }
+  return ILS_OK;
+}
+
+template <typename T>
+ils_status solve_t(const ils_plan* p, const T* f, const T* mx, const T* my, T* u, int64_t ps, void* ws,
+                   cudaStream_t s, int32_t* status) {
+  cx<T>* Sa = static_cast<cx<T>*>(ws);
+  ILS_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t), s));
+  RowArgs<T> a = row_args<T>(p);
+  a.f = f;
+  a.mux = mx;
+  a.muy = my;
+  a.f_ps = ps;
+  a.f_rp = p->W;
+  a.u = u;
+  a.u_ps = ps;
+  a.u_rp = p->W;
+  a.status = status;
+  a.iter = 1;
+  a.Sout = Sa;
+  ILS_CUDA(launch_row<T>(p, MODE_MU, a, s));
+  ILS_CUDA(launch_col<T>(p, col_args<T>(p, Sa, COL_SOLVE), s));
+  a.Sin = Sa;
+  a.Sout = nullptr;
+  a.f = nullptr;
+  ILS_CUDA(launch_row<T>(p, MODE_FIN, a, s));
+  return ILS_OK;
+}
+
+ils_status validate(const ils_params* q) {
+  if (!q) return fail(ILS_EINVAL, "params is NULL");
+  if (!(q->lam > 0.0 && std::isfinite(q->lam))) return fail(ILS_EINVAL, "lam must be finite and positive, got %g", q->lam);
+  if (q->iters < 1) return fail(ILS_EINVAL, "iters must be an integer >= 1, got %d", q->iters);
+  double c0;
+  if (q->kind == ILS_CHARBONNIER) {
+    if (!(q->p > 0.0 && q->p <= 1.0)) return fail(ILS_EINVAL, "p must be in (0,1]");
+    if (!(q->eps > 0.0)) return fail(ILS_EINVAL, "eps must be positive, got %g", q->eps);
+    c0 = q->p * std::pow(q->eps, q->p / 2.0 - 1.0);
+  } else if (q->kind == ILS_WELSCH) {
+    if (!(q->gamma > 0.0)) return fail(ILS_EINVAL, "gamma must be positive, got %g", q->gamma);
+    c0 = 2.0;
+  } else {
+    return fail(ILS_EINVAL, "unknown penalty kind %d", q->kind);
+  }
+  if (!std::isfinite(q->c) || q->c < c0 * (1.0 - 1e-12))
+    return fail(ILS_EINVAL, "c=%.17g is below the penalty's minimum curvature %.17g", q->c, c0);
+  return ILS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ils_abi_version(void) { return ILS_ABI_VERSION; }
+const char* ils_last_error(void) { return g_err.c_str(); }
+
+ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_t width, const ils_params* params,
+                           int32_t dtype, int32_t device) {
+  if (!out) return fail(ILS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (batch < 1) return fail(ILS_EINVAL, "batch must be >= 1, got %d", batch);
+  if (height < 1 || width < 1) return fail(ILS_EINVAL, "invalid plan size %dx%d", height, width);
+  if (dtype != ILS_F32 && dtype != ILS_F64) return fail(ILS_EINVAL, "unknown dtype %d", dtype);
+  ils_status st = validate(params);
+  if (st != ILS_OK) return st;
+  if (has_big_prime(height) || has_big_prime(width % 2 == 0 ? width / 2 : width))
+    return fail(ILS_EUNSUPPORTED, "plane size %dx%d has a prime factor > %d (unsupported FFT length)", height, width,
+                kMaxGenericPrime);
+  ils_plan* p = new ils_plan();
+  p->B = batch;
+  p->H = height;
+  p->W = width;
+  p->packed = (width % 2 == 0);
+  p->N = p->packed ? width / 2 : width;
+  p->Wc = width / 2 + 1;
+  p->Sp = (p->Wc + 1) & ~1;
+  p->dtype = dtype;
+  p->device = device;
+  p->prm = *params;
+  const size_t elt = dtype == ILS_F32 ? sizeof(cx<float>) : sizeof(cx<double>);
+  const int maxe = dtype == ILS_F32 ? 16 : 8;
+  if (!choose_row(*p, maxe, elt) || !choose_col(*p, maxe, elt)) {
+    delete p;
+    return fail(ILS_EUNSUPPORTED, "no launch configuration fits plane size %dx%d", height, width);
+  }
+  // device tables: row twiddles, col twiddles, wreal, wx, wy (all in T)
+  const size_t rs = dtype == ILS_F32 ? 4 : 8;
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off = 0;
+  p->off_rowtw = off;
+  off = align(off + p->rowf.tw.size() * rs);
+  p->off_coltw = off;
+  off = align(off + p->colf.tw.size() * rs);
+  p->off_wreal = off;
+  const int nwr = p->N / 2 + 1;
+  off = align(off + 2 * nwr * rs);
+  p->off_wx = off;
+  off = align(off + p->Wc * rs);
+  p->off_wy = off;
+  off = align(off + p->H * rs);
+  p->off_sink = off;  // scratch status word for ils_irfft2
+  off += 256;
+  std::vector<double> host(off / 8 + 1, 0.0);
+  std::vector<char> bytes(off, 0);
+  auto put = [&](size_t o, const std::vector<double>& v) {
+    if (dtype == ILS_F64) {
+      memcpy(bytes.data() + o, v.data(), v.size() * 8);
+    } else {
+      std::vector<float> f(v.begin(), v.end());
+      memcpy(bytes.data() + o, f.data(), f.size() * 4);
+    }
+  };
+  put(p->off_rowtw, p->rowf.tw);
+  put(p->off_coltw, p->colf.tw);
+  std::vector<double> wr(2 * nwr), wx(p->Wc), wy(p->H);
+  for (int k = 0; k < nwr; ++k) {
+    const sc_t w = sincos2pi(-k, width);
+    wr[2 * k] = w.c;
+    wr[2 * k + 1] = w.s;
+  }
+  // w = 2 - 2 cos(2 pi k / n): solver.py:100-101
+  for (int k = 0; k < p->Wc; ++k) wx[k] = 2.0 - 2.0 * sincos2pi(k, width).c;
+  for (int k = 0; k < p->H; ++k) wy[k] = 2.0 - 2.0 * sincos2pi(k, height).c;
+  put(p->off_wreal, wr);
+  put(p->off_wx, wx);
+  put(p->off_wy, wy);
+  p->spec_bytes = ((size_t)batch * height * p->Sp * elt + 255) & ~size_t(255);
+  p->epart_elems = (size_t)(params->iters + 1) * batch * p->row_grid;
+  if (device < 0) {  // host-only plan: planning/introspection, cannot run
+    *out = p;
+    return ILS_OK;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_tables, off);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_tables, bytes.data(), off, cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    if (p->d_tables) cudaFree(p->d_tables);
+    delete p;
+    return fail(ILS_ECUDA, "plan tables: %s", cudaGetErrorString(e));
+  }
+  *out = p;
+  return ILS_OK;
+}
+
+void ils_plan_destroy(ils_plan* p) {
+  if (!p) return;
+  if (p->d_tables) cudaFree(p->d_tables);
+  delete p;
+}
+
+ils_status ils_workspace_size(const ils_plan* p, size_t* bytes) {
+  if (!p || !bytes) return fail(ILS_EINVAL, "NULL argument");
+  *bytes = 2 * p->spec_bytes + 256 + p->epart_elems * sizeof(double);  // [Sa][Sb][status][trace partials]
+  return ILS_OK;
+}
+
+ils_status ils_plan_get_info(const ils_plan* p, ils_plan_info* i) {
+  if (!p || !i) return fail(ILS_EINVAL, "NULL argument");
+  memset(i, 0, sizeof *i);
+  i->batch = p->B;
+  i->height = p->H;
+  i->width = p->W;
+  i->dtype = p->dtype;
+  i->packed = p->packed;
+  i->row_band = p->band;
+  i->row_threads = p->row_threads;
+  i->row_group = p->rowf.G;
+  i->col_group = p->colf.G;
+  i->row_spec = p->row_spec;
+  i->col_spec = p->col_spec;
+  i->row_grid = p->row_grid;
+  i->row_smem = (int32_t)p->row_smem;
+  i->col_cols = p->C;
+  i->col_threads = p->col_threads;
+  i->col_grid = p->col_grid;
+  i->col_smem = (int32_t)p->col_smem;
+  i->row_passes = (int32_t)p->rowf.radix.size();
+  i->col_passes = (int32_t)p->colf.radix.size();
+  for (size_t k = 0; k < p->rowf.radix.size() && k < 16; ++k) i->row_radix[k] = p->rowf.radix[k];
+  for (size_t k = 0; k < p->colf.radix.size() && k < 16; ++k) i->col_radix[k] = p->colf.radix[k];
+  i->spec_pitch = p->Sp;
+  i->launches_per_call = 2 * p->prm.iters + 1;
+  return ILS_OK;
+}
+
+ils_status ils_smooth(const ils_plan* p, const void* f, void* u, int64_t ps, void* ws, void* stream, int32_t* status,
+                      double* energies) {
+  if (!p || !f || !u || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->dtype == ILS_F32)
+    return smooth_t<float>(p, static_cast<const float*>(f), static_cast<float*>(u), ps, ws, s, status, energies);
+  return smooth_t<double>(p, static_cast<const double*>(f), static_cast<double*>(u), ps, ws, s, status, energies);
+}
+
+ils_status ils_solve_ls(const ils_plan* p, const void* f, const void* mx, const void* my, void* u, int64_t ps,
+                        void* ws, void* stream, int32_t* status) {
+  if (!p || !f || !mx || !my || !u || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->dtype == ILS_F32)
+    return solve_t<float>(p, static_cast<const float*>(f), static_cast<const float*>(mx),
+                          static_cast<const float*>(my), static_cast<float*>(u), ps, ws, s, status);
+  return solve_t<double>(p, static_cast<const double*>(f), static_cast<const double*>(mx),
+                         static_cast<const double*>(my), static_cast<double*>(u), ps, ws, s, status);
+}
+
+ils_status ils_host_io_size(const ils_plan* p, size_t* bytes) {
+  if (!p || !bytes) return fail(ILS_EINVAL, "NULL argument");
+  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
+  const size_t batch_bytes = ((size_t)p->B * p->H * p->W * es + 255) & ~size_t(255);
+  *bytes = 4 * batch_bytes + 256;  // 2 slots x (f, u) + 2 status words
+  return ILS_OK;
+}
+
+ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, int64_t ps, int32_t nbatches,
+                           void* ws, void* io_dev, void* stream, int32_t* bad_iter) {
+  if (!p || !f_host || !u_host || !ws || !io_dev) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
+  if (ps != (int64_t)p->H * p->W) return fail(ILS_EINVAL, "host planes must be dense (plane_stride == H*W)");
+  if (bad_iter) *bad_iter = -1;
+  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
+  const size_t bytes = (size_t)p->B * ps * es;
+  const size_t slot = (bytes + 255) & ~size_t(255);
+  char* io = static_cast<char*>(io_dev);
+  char* fslot[2] = {io, io + slot};
+  char* uslot[2] = {io + 2 * slot, io + 3 * slot};
+  int32_t* st[2] = {reinterpret_cast<int32_t*>(io + 4 * slot), reinterpret_cast<int32_t*>(io + 4 * slot + 128)};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  int32_t* hstat = nullptr;
+  ils_status rc = ILS_OK;
+  auto cleanup = [&]() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+      if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+      if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+    }
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
+    if (hstat) cudaFreeHost(hstat);
+  };
+#define ILS_TRY(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      rc = fail(ILS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));                     \
+      cleanup();                                                                         \
+      return rc;                                                                         \
+    }                                                                                    \
+  } while (0)
+  ILS_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  ILS_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    ILS_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    ILS_TRY(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
+    ILS_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+  }
+  ILS_TRY(cudaHostAlloc(reinterpret_cast<void**>(&hstat), sizeof(int32_t) * nbatches, cudaHostAllocDefault));
+  // the caller's stream may still be producing host-visible state: order h2d after it
+  ILS_TRY(cudaEventRecord(ev_out[0], s));
+  ILS_TRY(cudaStreamWaitEvent(h2d, ev_out[0], 0));
+  ILS_TRY(cudaStreamWaitEvent(d2h, ev_out[0], 0));
+  for (int k = 0; k < nbatches; ++k) {
+    const int sl = k & 1;
+    const char* fh = static_cast<const char*>(f_host) + (size_t)k * bytes;
+    char* uh = static_cast<char*>(u_host) + (size_t)k * bytes;
+    if (k >= 2) ILS_TRY(cudaStreamWaitEvent(h2d, ev_comp[sl], 0));  // f slot consumed by batch k-2
+    ILS_TRY(cudaMemcpyAsync(fslot[sl], fh, bytes, cudaMemcpyHostToDevice, h2d));
+    ILS_TRY(cudaEventRecord(ev_in[sl], h2d));
+    ILS_TRY(cudaStreamWaitEvent(s, ev_in[sl], 0));
+    if (k >= 2) ILS_TRY(cudaStreamWaitEvent(s, ev_out[sl], 0));  // u slot drained by batch k-2
+    ils_status r = ils_smooth(p, fslot[sl], uslot[sl], ps, ws, stream, st[sl], nullptr);
+    if (r != ILS_OK) {
+      cleanup();
+      return r;
+    }
+    ILS_TRY(cudaEventRecord(ev_comp[sl], s));
+    ILS_TRY(cudaStreamWaitEvent(d2h, ev_comp[sl], 0));
+    ILS_TRY(cudaMemcpyAsync(uh, uslot[sl], bytes, cudaMemcpyDeviceToHost, d2h));
+    ILS_TRY(cudaMemcpyAsync(hstat + k, st[sl], sizeof(int32_t), cudaMemcpyDeviceToHost, d2h));
+    ILS_TRY(cudaEventRecord(ev_out[sl], d2h));
+  }
+  ILS_TRY(cudaStreamSynchronize(d2h));
+  ILS_TRY(cudaStreamSynchronize(s));
+#undef ILS_TRY
+  int worst = ILS_STATUS_CLEAN;
+  for (int k = 0; k < nbatches; ++k) worst = std::min(worst, (int)hstat[k]);
+  cleanup();
+  if (worst != ILS_STATUS_CLEAN) {
+    if (bad_iter) *bad_iter = worst;
+    if (worst == 0) return fail(ILS_ENONFINITE_INPUT, "image plane contains non-finite values");
+    return fail(ILS_ENONFINITE, "non-finite iterate at iteration %d", worst);
+  }
+  return ILS_OK;
+}
+
+ils_status ils_launch_pass(const ils_plan* p, int32_t pass, const void* f, void* u, int64_t ps, void* ws,
+                           void* stream, int32_t* status) {
+  if (!p || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (pass < 0 || pass > 3) return fail(ILS_EINVAL, "pass must be 0..3, got %d", pass);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto run = [&](auto tag) -> ils_status {
+    using T = decltype(tag);
+    cx<T>* Sa = static_cast<cx<T>*>(ws);
+    cx<T>* Sb = reinterpret_cast<cx<T>*>(static_cast<char*>(ws) + p->spec_bytes);
+    if (pass == 1) {
+      ILS_CUDA(launch_col<T>(p, col_args<T>(p, Sa, COL_SOLVE), s));
+      return ILS_OK;
+    }
+    RowArgs<T> a = row_args<T>(p);
+    a.f = static_cast<const T*>(f);
+    a.f_ps = ps;
+    a.f_rp = p->W;
+    a.u = static_cast<T*>(u);
+    a.u_ps = ps;
+    a.u_rp = p->W;
+    a.status = status;
+    a.iter = pass == 3 ? p->prm.iters : 1;
+    a.Sin = Sa;
+    a.Sout = pass == 0 ? Sa : Sb;
+    const int mode = pass == 0 ? MODE_F0 : (pass == 2 ? MODE_IT : MODE_FIN);
+    ILS_CUDA(launch_row<T>(p, mode, a, s));
+    return ILS_OK;
+  };
+  return p->dtype == ILS_F32 ? run(float{}) : run(double{});
+}
+
+ils_status ils_rfft2(const ils_plan* p, const void* x, int64_t ps, void* spec, int64_t pitch, void* stream) {
+  if (!p || !x || !spec) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (pitch < p->Wc) return fail(ILS_EINVAL, "spec_pitch %lld < width/2+1", (long long)pitch);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto run = [&](auto tag) -> ils_status {
+    using T = decltype(tag);
+    RowArgs<T> a = row_args<T>(p);
+    a.f = static_cast<const T*>(x);
+    a.f_ps = ps;
+    a.f_rp = p->W;
+    a.Sout = static_cast<cx<T>*>(spec);
+    a.S_rp = (int)pitch;
+    a.S_ps = (long long)p->H * pitch;
+    ILS_CUDA(launch_row<T>(p, MODE_R2C, a, s));
+    ColArgs<T> c = col_args<T>(p, static_cast<cx<T>*>(spec), COL_FWD);
+    c.S_rp = (int)pitch;
+    c.S_ps = (long long)p->H * pitch;
+    ILS_CUDA(launch_col<T>(p, c, s));
+    return ILS_OK;
+  };
+  return p->dtype == ILS_F32 ? run(float{}) : run(double{});
+}
+
+ils_status ils_irfft2(const ils_plan* p, void* spec, int64_t pitch, void* x, int64_t ps, void* stream) {
+  if (!p || !x || !spec) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (pitch < p->Wc) return fail(ILS_EINVAL, "spec_pitch %lld < width/2+1", (long long)pitch);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto run = [&](auto tag) -> ils_status {
+    using T = decltype(tag);
+    ColArgs<T> c = col_args<T>(p, static_cast<cx<T>*>(spec), COL_INV);
+    c.S_rp = (int)pitch;
+    c.S_ps = (long long)p->H * pitch;
+    ILS_CUDA(launch_col<T>(p, c, s));
+    RowArgs<T> a = row_args<T>(p);
+    a.Sin = static_cast<const cx<T>*>(spec);
+    a.S_rp = (int)pitch;
+    a.S_ps = (long long)p->H * pitch;
+    a.u = static_cast<T*>(x);
+    a.u_ps = ps;
+    a.u_rp = p->W;
+    a.iter = 1;
+    a.status = reinterpret_cast<int*>(static_cast<char*>(p->d_tables) + p->off_sink);
+    ILS_CUDA(launch_row<T>(p, MODE_FIN, a, s));
+    return ILS_OK;
+  };
+  return p->dtype == ILS_F32 ? run(float{}) : run(double{});
+}
+
+ils_status ils_rgb_yuv(void* planes, int32_t dtype, int64_t ps, int64_t npx, int32_t frames, int32_t inverse,
+                       void* stream) {
+  if (!planes || frames < 1 || npx < 1 || ps < npx) return fail(ILS_EINVAL, "bad rgb_yuv arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long n = npx * frames;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+  if (dtype == ILS_F32)
+    k_rgb_yuv<float><<<blocks, 256, 0, s>>>(static_cast<float*>(planes), ps, npx, frames, inverse);
+  else
+    k_rgb_yuv<double><<<blocks, 256, 0, s>>>(static_cast<double*>(planes), ps, npx, frames, inverse);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+}  // extern "C"

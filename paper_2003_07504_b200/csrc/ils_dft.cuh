@@ -1,0 +1,218 @@
+// Register-resident small DFTs (radix butterflies) for the ILS FFT engine.
+//
+// Replaces the inner arithmetic of scipy.fft.fft2/ifft2 that the reference
+// calls through solver.py:24-30.  Everything here is compile-time shaped:
+// a radix-R DFT over R complex values held in registers, with every twiddle
+// a constexpr folded into the instruction stream.  Composite radices are
+// built by Cooley-Tukey from 2, 4 and odd primes (3, 5, 7, 11, 13).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+#include <utility>
+
+namespace ils {
+
+template <typename T>
+struct alignas(2 * sizeof(T)) cx {
+  T x, y;
+};
+
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> operator+(cx<T> a, cx<T> b) { return {a.x + b.x, a.y + b.y}; }
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> operator-(cx<T> a, cx<T> b) { return {a.x - b.x, a.y - b.y}; }
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> cmul(cx<T> a, cx<T> b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+// a * conj(b)
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> cmulc(cx<T> a, cx<T> b) {
+  return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
+}
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> conj(cx<T> a) { return {a.x, -a.y}; }
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> scale(cx<T> a, T s) { return {a.x * s, a.y * s}; }
+
+// ------------------------------------------------------------ constexpr trig
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+struct sc_t {
+  double s, c;
+};
+
+__host__ __device__ constexpr double ct_sin_small(double x) {
+  double x2 = x * x, term = x, sum = x;
+  for (int n = 1; n < 14; ++n) {
+    term *= -x2 / double((2 * n) * (2 * n + 1));
+    sum += term;
+  }
+  return sum;
+}
+__host__ __device__ constexpr double ct_cos_small(double x) {
+  double x2 = x * x, term = 1.0, sum = 1.0;
+  for (int n = 1; n < 14; ++n) {
+    term *= -x2 / double((2 * n - 1) * (2 * n));
+    sum += term;
+  }
+  return sum;
+}
+// sin/cos of 2*pi*num/den with exact integer octant reduction (|arg| <= pi/4
+// for the series), so table entries are correct to ~1 ulp in double.
+__host__ __device__ constexpr sc_t sincos2pi(long long num, long long den) {
+  long long m = ((num % den) + den) % den;
+  long long q = (4 * m) / den;       // quadrant
+  long long r = 4 * m - q * den;     // angle inside quadrant = (pi/2) r / den
+  bool swap = 2 * r > den;
+  double x = swap ? (kPi / 2) * double(den - r) / double(den) : (kPi / 2) * double(r) / double(den);
+  double sx = ct_sin_small(x), cx_ = ct_cos_small(x);
+  double s0 = swap ? cx_ : sx, c0 = swap ? sx : cx_;
+  sc_t out{0.0, 0.0};
+  if (q == 0) out = {s0, c0};
+  else if (q == 1) out = {c0, -s0};
+  else if (q == 2) out = {-s0, -c0};
+  else out = {-c0, s0};
+  return out;
+}
+
+// ------------------------------------------------------------ static for
+template <int... Is, class F>
+__device__ __forceinline__ void sfor_impl(std::integer_sequence<int, Is...>, F&& f) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (N > 0) sfor_impl(std::make_integer_sequence<int, N>{}, static_cast<F&&>(f));
+}
+#define ILS_CV(I) (decltype(I)::value)
+
+// ------------------------------------------------------------ radix helpers
+template <int R>
+constexpr bool ct_is_prime() {
+  if (R < 2) return false;
+  for (int d = 2; d * d <= R; ++d)
+    if (R % d == 0) return false;
+  return true;
+}
+constexpr int split_of(int r) {
+  int best = r;
+  if (r % 4 == 0 && r > 4) {
+    best = 4;
+  } else {
+    int p = 2;
+    while (p < r && r % p != 0) ++p;
+    best = p;
+  }
+  return best;
+}
+template <int R>
+constexpr int ct_split() {
+  return split_of(R);
+}
+
+// Multiply by w = exp(DIR * 2*pi*i * K / R), specialised for quarter turns.
+template <int K, int R, int DIR, typename T>
+__device__ __forceinline__ cx<T> twc(cx<T> a) {
+  constexpr int k = ((K % R) + R) % R;
+  if constexpr (k == 0) {
+    return a;
+  } else if constexpr ((4 * k) % R == 0) {
+    constexpr int q = (4 * k) / R;
+    constexpr int qq = (DIR > 0) ? q : (4 - q) % 4;
+    if constexpr (qq == 1) return cx<T>{-a.y, a.x};
+    else if constexpr (qq == 2) return cx<T>{-a.x, -a.y};
+    else return cx<T>{a.y, -a.x};
+  } else {
+    constexpr sc_t w = sincos2pi(DIR * k, R);
+    const T c = T(w.c), s = T(w.s);
+    return cx<T>{a.x * c - a.y * s, a.x * s + a.y * c};
+  }
+}
+
+template <int R, int DIR, typename T>
+__device__ __forceinline__ void dft(cx<T>* v);
+
+// Odd prime: symmetric direct form, (R-1)^2/2 real FMAs per component.
+template <int R, int DIR, typename T>
+__device__ __forceinline__ void dft_prime(cx<T>* v) {
+  constexpr int h = (R - 1) / 2;
+  cx<T> s[h], d[h];
+  sfor<h>([&](auto I) {
+    constexpr int n = ILS_CV(I) + 1;
+    s[ILS_CV(I)] = v[n] + v[R - n];
+    d[ILS_CV(I)] = v[n] - v[R - n];
+  });
+  const cx<T> x0 = v[0];
+  cx<T> X0 = x0;
+  sfor<h>([&](auto I) { X0 = X0 + s[ILS_CV(I)]; });
+  cx<T> out[R];
+  out[0] = X0;
+  sfor<h>([&](auto K) {
+    constexpr int k = ILS_CV(K) + 1;
+    cx<T> a = x0, b{T(0), T(0)};
+    sfor<h>([&](auto I) {
+      constexpr int n = ILS_CV(I) + 1;
+      constexpr sc_t w = sincos2pi((long long)(n * k) % R, R);
+      const T c = T(w.c), sn = T(w.s);
+      a.x += s[ILS_CV(I)].x * c;
+      a.y += s[ILS_CV(I)].y * c;
+      b.x += d[ILS_CV(I)].x * sn;
+      b.y += d[ILS_CV(I)].y * sn;
+    });
+    const cx<T> ib = (DIR > 0) ? cx<T>{-b.y, b.x} : cx<T>{b.y, -b.x};
+    out[k] = a + ib;
+    out[R - k] = a - ib;
+  });
+  sfor<R>([&](auto I) { v[ILS_CV(I)] = out[ILS_CV(I)]; });
+}
+
+// Composite: R = A*B, n = B*n1 + n2, k = k1 + A*k2.
+template <int R, int DIR, typename T>
+__device__ __forceinline__ void dft_ct(cx<T>* v) {
+  constexpr int A = ct_split<R>(), B = R / A;
+  sfor<B>([&](auto N2) {
+    constexpr int n2 = ILS_CV(N2);
+    cx<T> t[A];
+    sfor<A>([&](auto N1) { t[ILS_CV(N1)] = v[B * ILS_CV(N1) + n2]; });
+    dft<A, DIR>(t);
+    sfor<A>([&](auto K1) {
+      constexpr int k1 = ILS_CV(K1);
+      v[B * k1 + n2] = twc<n2 * k1, R, DIR>(t[k1]);
+    });
+  });
+  sfor<A>([&](auto K1) { dft<B, DIR>(v + B * ILS_CV(K1)); });
+  cx<T> o[R];
+  sfor<A>([&](auto K1) {
+    sfor<B>([&](auto K2) { o[ILS_CV(K1) + A * ILS_CV(K2)] = v[B * ILS_CV(K1) + ILS_CV(K2)]; });
+  });
+  sfor<R>([&](auto I) { v[ILS_CV(I)] = o[ILS_CV(I)]; });
+}
+
+// X[k] = sum_n v[n] exp(DIR * 2*pi*i*n*k/R), unnormalised, in place.
+template <int R, int DIR, typename T>
+__device__ __forceinline__ void dft(cx<T>* v) {
+  if constexpr (R == 1) {
+    return;
+  } else if constexpr (R == 2) {
+    const cx<T> a = v[0], b = v[1];
+    v[0] = a + b;
+    v[1] = a - b;
+  } else if constexpr (R == 4) {
+    const cx<T> a0 = v[0] + v[2], a1 = v[0] - v[2], a2 = v[1] + v[3];
+    const cx<T> d = v[1] - v[3];
+    const cx<T> a3 = (DIR > 0) ? cx<T>{-d.y, d.x} : cx<T>{d.y, -d.x};
+    v[0] = a0 + a2;
+    v[2] = a0 - a2;
+    v[1] = a1 + a3;
+    v[3] = a1 - a3;
+  } else if constexpr (ct_is_prime<R>()) {
+    dft_prime<R, DIR>(v);
+  } else {
+    dft_ct<R, DIR>(v);
+  }
+}
+
+}  // namespace ils

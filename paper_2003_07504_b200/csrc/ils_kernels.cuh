@@ -1,0 +1,526 @@
+// ILS hot-path kernels (sm_100a): the fused row pass and the column pass.
+//
+// One ILS iteration (reference smoother.py:162-169 -> penalty.py:117-126,
+// solver.py:33-49 and solver.py:109-134) is two launches over a half
+// spectrum S[B][H][Sp] (complex, row-major, the layout of rfft2):
+//
+//   k_row  (band of rows + 1 halo row each side):
+//          S rows --c2r--> u rows (smem) --stencil--> rhs = f + lam/2 D^T mu
+//          --r2c--> S rows          (mu = c*Du - phi'(Du), never materialised)
+//   k_col  (strip of columns): forward column FFT, * 1/(H W denom), inverse
+//          column FFT, in place.  denom = 1 + c lam/2 (wy[ky] + wx[kx]) is
+//          evaluated from two 1-D tables (solver.py:100-102).
+//
+// Iteration 0 reads f directly (u0 = f); the final row pass (k_row with
+// MODE_FIN) writes u.  F(f) is never needed: f is added in the spatial
+// domain (linearity), so every iteration moves (S in, f in, S out) + (S in,
+// S out) = 20 bytes per pixel for fp32.
+#pragma once
+
+#include "ils_fft.cuh"
+
+namespace ils {
+
+enum RowMode : int {
+  MODE_F0 = 0,   // u = f                     -> stencil -> r2c -> S
+  MODE_IT = 1,   // u = c2r(S_in)             -> stencil -> r2c -> S_out
+  MODE_MU = 2,   // rhs = f + lam/2 D^T(mu_x, mu_y) (solve_ls) -> r2c -> S
+  MODE_FIN = 3,  // u = c2r(S_in) -> u_out
+  MODE_R2C = 4,  // rhs = f -> r2c -> S  (rfft2)
+};
+
+enum ColMode : int { COL_SOLVE = 0, COL_FWD = 1, COL_INV = 2 };
+
+constexpr int kStatusClean = 0x7f7f7f7f;  // cudaMemset(0x7f) pattern
+
+template <typename T>
+struct PenaltyDev {
+  int kind;   // 0 Charbonnier, 1 Welsch
+  T p;        // Charbonnier exponent
+  T pe;       // p/2 - 1
+  T ph;       // p/2
+  T eps;
+  T wk;       // Welsch: -1/(2 g^2)  (natural-log scale)
+  T g2x2;     // Welsch: 2 g^2
+  T c;        // curvature
+  T lam;
+  T lam2;     // lam / 2
+};
+
+template <typename T>
+struct RowArgs {
+  int mode;  // RowMode
+  int B, H, W, N, Wc, band, LP;
+  const T* f;
+  long long f_ps;
+  int f_rp;
+  const T* mux;
+  const T* muy;
+  const cx<T>* Sin;
+  cx<T>* Sout;
+  long long S_ps;
+  int S_rp;
+  T* u;
+  long long u_ps;
+  int u_rp;
+  PenaltyDev<T> pen;
+  int iter;          // iteration index of the u held by this pass
+  int* status;       // atomicMin(first bad iteration); 0 = non-finite input
+  double* epart;     // energy partials [B][gridDim.x] or nullptr
+  FftDev<T> fft;     // row transform (length N = W/2 packed, W otherwise)
+  const cx<T>* wreal;  // exp(-2 pi i k / W), k = 0..N/2 (packed only)
+};
+
+template <typename T>
+struct ColArgs {
+  int B, H, Wc, C, CS;
+  cx<T>* S;
+  long long S_ps;
+  int S_rp;
+  const T* wx;  // 2 - 2 cos(2 pi kx / W), kx < Wc
+  const T* wy;  // 2 - 2 cos(2 pi ky / H)
+  T cl2;        // c * lam / 2
+  T inv_hw;     // 1 / (H W)
+  int mode;
+  FftDev<T> fft;
+};
+
+// ------------------------------------------------------------ penalty math
+__device__ __forceinline__ float fpow_pos(float q, float e) { return exp2f(e * __log2f(q)); }
+__device__ __forceinline__ double fpow_pos(double q, double e) { return pow(q, e); }
+__device__ __forceinline__ float fexp(float x) { return __expf(x); }
+__device__ __forceinline__ double fexp(double x) { return exp(x); }
+
+// phi'(x): penalty.py:64-66 (Charbonnier), 93-96 (Welsch)
+template <typename T>
+__device__ __forceinline__ T dphi(T x, const PenaltyDev<T>& P) {
+  if (P.kind == 0) return P.p * x * fpow_pos(x * x + P.eps, P.pe);
+  return T(2) * x * fexp(x * x * P.wk);
+}
+// phi(x): penalty.py:60-62, 88-91 (trace only)
+template <typename T>
+__device__ __forceinline__ T phi(T x, const PenaltyDev<T>& P) {
+  if (P.kind == 0) return fpow_pos(x * x + P.eps, P.ph);
+  return P.g2x2 * (T(1) - fexp(x * x * P.wk));
+}
+// mu = c x - phi'(x): penalty.py:117-126
+template <typename T>
+__device__ __forceinline__ T aux(T x, const PenaltyDev<T>& P) {
+  return P.c * x - dphi(x, P);
+}
+
+template <typename T>
+__device__ __forceinline__ bool finite_(T v) { return isfinite(v); }
+
+// ------------------------------------------------------------ line access
+// Line i of a row CTA starts at lines + i*LP (complex slots, padded).  In a
+// packed line, real sample x lives in complex slot x>>1, component x&1.
+template <typename T, bool PACKED>
+struct Lines {
+  cx<T>* base;
+  int LP;
+  __device__ __forceinline__ cx<T>* line(int i) const { return base + (size_t)i * LP; }
+  __device__ __forceinline__ T get(int i, int x) const {
+    if (PACKED) return reinterpret_cast<const T*>(line(i))[2 * pad<T>(x >> 1) + (x & 1)];
+    return line(i)[pad<T>(x)].x;
+  }
+  __device__ __forceinline__ void set(int i, int x, T v) const {
+    if (PACKED) reinterpret_cast<T*>(line(i))[2 * pad<T>(x >> 1) + (x & 1)] = v;
+    else line(i)[pad<T>(x)] = cx<T>{v, T(0)};
+  }
+};
+
+__device__ __forceinline__ int wrapi(int x, int n) { return x < 0 ? x + n : (x >= n ? x - n : x); }
+
+// Deterministic block sum (fixed shuffle tree + fixed warp order).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) s += red[i];
+  }
+  __syncthreads();
+  return s;
+}
+
+// ------------------------------------------------------------ real <-> half-complex packing
+// Forward post-process of one packed line: Z = FFT_N(x[2n] + i x[2n+1]) ->
+// X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
+// O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to slot N.
+template <typename T>
+__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Group& g) {
+  for (int k = g.rank; k <= N / 2; k += g.size) {
+    if (k == 0) {
+      const cx<T> z0 = z[0];
+      z[0] = cx<T>{z0.x + z0.y, T(0)};
+      z[pad<T>(N)] = cx<T>{z0.x - z0.y, T(0)};
+    } else {
+      const cx<T> zk = z[pad<T>(k)], zm = z[pad<T>(N - k)];
+      const cx<T> E{T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y)};
+      const cx<T> d{T(0.5) * (zk.x - zm.x), T(0.5) * (zk.y + zm.y)};  // (zk - conj zm)/2
+      const cx<T> O{d.y, -d.x};                                          // -i * d
+      const cx<T> wO = cmul(ldg_cx(wreal + k), O);
+      z[pad<T>(k)] = E + wO;
+      if (N - k != k) z[pad<T>(N - k)] = conj(E - wO);
+    }
+  }
+  g.sync();
+}
+
+// Inverse pre-process: Z_k = E + iO, Z_{N-k} = conj(E) + i conj(O) with
+// E = X_k + conj X_{N-k}, O = (X_k - conj X_{N-k}) conj(w^k).  An inverse
+// N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
+template <typename T>
+__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Group& g) {
+  for (int k = g.rank; k <= N / 2; k += g.size) {
+    if (k == 0) {
+      const T a = z[0].x, c = z[pad<T>(N)].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
+      z[0] = cx<T>{a + c, a - c};
+    } else {
+      const cx<T> xk = z[pad<T>(k)], xm = z[pad<T>(N - k)];
+      const cx<T> E{xk.x + xm.x, xk.y - xm.y};
+      const cx<T> D{xk.x - xm.x, xk.y + xm.y};
+      const cx<T> O = cmulc(D, ldg_cx(wreal + k));
+      z[pad<T>(k)] = cx<T>{E.x - O.y, E.y + O.x};
+      if (N - k != k) z[pad<T>(N - k)] = cx<T>{E.x + O.y, -E.y + O.x};
+    }
+  }
+  g.sync();
+}
+
+// ------------------------------------------------------------ row pass
+constexpr int kRowThreads = 256;
+constexpr int kNarrowMaxW = 4 * 4 * kRowThreads;  // stencil: 4 strips x 4 columns per thread
+constexpr int kWideMaxW = 4 * 8 * kRowThreads;
+constexpr int kColThreads = 256;
+
+template <typename T, bool PACKED, class FS, bool WIDE>
+__global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  const int MODE = A.mode;  // block-uniform
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const Group g{tid / A.fft.G, A.fft.G, tid % A.fft.G};
+  const int ngroups = nthr / A.fft.G;
+  const int b = blockIdx.y;
+  const int r0 = blockIdx.x * A.band;
+  const int nb = min(A.band, A.H - r0);
+  const int W = A.W, H = A.H;
+  const bool trace = A.epart != nullptr;
+  const bool halo = (MODE == MODE_F0 || MODE == MODE_IT || (MODE == MODE_FIN && trace));
+  const int nl = halo ? nb + 2 : nb;
+  const int y0 = halo ? r0 - 1 : r0;
+  const int off = halo ? 1 : 0;
+  const Lines<T, PACKED> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP};
+  const PenaltyDev<T>& P = A.pen;
+  const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
+
+  if (MODE == MODE_MU || MODE == MODE_R2C) {
+    // rhs rows straight from global memory; each group owns whole lines.
+    bool bf = false, bx = false, by = false;
+    const T* mx = A.mux ? A.mux + (size_t)b * A.f_ps : nullptr;
+    const T* my = A.muy ? A.muy + (size_t)b * A.f_ps : nullptr;
+    for (int i = g.id; i < nb; i += ngroups) {
+      const int r = r0 + i;
+      for (int x = g.rank; x < W; x += g.size) {
+        const size_t o = (size_t)r * A.f_rp + x;
+        T v = fpl[o];
+        bf |= !finite_(v);
+        if (MODE == MODE_MU) {
+          // rhs = f + lam/2 (mu_x[r,x-1] - mu_x[r,x] + mu_y[r-1,x] - mu_y[r,x]): solver.py:43-49, 127-129
+          const T mxc = mx[o], myc = my[o];
+          const T mxl = mx[(size_t)r * A.f_rp + wrapi(x - 1, W)];
+          const T myu = my[(size_t)wrapi(r - 1, H) * A.f_rp + x];
+          bx |= !finite_(mxc);
+          by |= !finite_(myc);
+          v = v + P.lam2 * ((mxl - mxc) + (myu - myc));
+        }
+        L.set(i, x, v);
+      }
+    }
+    if (MODE == MODE_MU) {
+      // solve_ls checks f, mu_x, mu_y in that order (solver.py:119-125)
+      const int fb = __syncthreads_or(bf), xb = __syncthreads_or(bx), yb = __syncthreads_or(by);
+      if (tid == 0) {
+        if (fb) atomicMin(A.status, 1);
+        if (xb) atomicMin(A.status, 2);
+        if (yb) atomicMin(A.status, 3);
+      }
+    } else {
+      __syncthreads();
+    }
+  } else {
+    // ---------------- phase A: u rows into shared memory (group per line)
+    bool bad = false;
+    for (int i = g.id; i < nl; i += ngroups) {
+      const int y = wrapi(y0 + i, H);
+      cx<T>* z = L.line(i);
+      if (MODE == MODE_F0) {
+        for (int x = g.rank; x < W; x += g.size) {
+          const T v = fpl[(size_t)y * A.f_rp + x];
+          if (i >= off && i < off + nb) bad |= !finite_(v);
+          L.set(i, x, v);
+        }
+      } else {
+        const cx<T>* src = A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp;
+        for (int k = g.rank; k < A.Wc; k += g.size) z[pad<T>(k)] = src[k];
+        g.sync();
+        if (PACKED) {
+          c2r_pre<T>(z, A.N, A.wreal, g);
+        } else {
+          // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
+          for (int k = A.Wc + g.rank; k < W; k += g.size) z[pad<T>(k)] = conj(z[pad<T>(W - k)]);
+          if (g.rank == 0) z[0].y = T(0);
+          g.sync();
+        }
+        fft_line<T, +1, FS>(z, A.fft, g);
+        if (i >= off && i < off + nb)
+          for (int x = g.rank; x < W; x += g.size) bad |= !finite_(L.get(i, x));
+      }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, MODE == MODE_F0 ? 0 : A.iter);
+
+    // ---------------- final pass: write u (and its energy)
+    if (MODE == MODE_FIN) {
+      double e = 0.0;
+      T* upl = A.u + (size_t)b * A.u_ps;
+      for (int t = tid; t < nb * W; t += nthr) {
+        const int j = t / W, x = t - j * W;
+        const T uc = L.get(j + off, x);
+        upl[(size_t)(r0 + j) * A.u_rp + x] = uc;
+        if (trace) {
+          const T gx = L.get(j + off, wrapi(x + 1, W)) - uc;
+          const T gy = L.get(j + off + 1, x) - uc;
+          const T d = uc - fpl[(size_t)(r0 + j) * A.f_rp + x];
+          e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
+        }
+      }
+      if (trace) {
+        const double s = block_sum(e, red);
+        if (tid == 0) A.epart[(size_t)b * gridDim.x + blockIdx.x] = s;
+      }
+      return;
+    }
+
+    // ---------------- phase B: fused stencil -> rhs rows (lines 0..nb-1)
+    // Each thread walks down a QW-column strip carrying mu_y of the row above
+    // in registers.  Line j+1 holds row r0+j; rhs of row r0+j is written into
+    // line j once every thread is past row r0+j-1.
+    constexpr int QW = WIDE ? 8 : 4, GMAX = 4;  // columns per strip, strips per thread
+    const int ng = (W + QW - 1) / QW;
+    T myup[GMAX][QW];
+    double e = 0.0;
+#pragma unroll
+    for (int gi = 0; gi < GMAX; ++gi) {
+      const int gg = tid + gi * nthr;
+      if (gg < ng) {
+#pragma unroll
+        for (int q = 0; q < QW; ++q) {
+          const int x = gg * QW + q;
+          if (x < W) myup[gi][q] = aux(L.get(1, x) - L.get(0, x), P);
+        }
+      }
+    }
+    for (int j = 0; j < nb; ++j) {
+      const int i = j + 1;
+      const T* frow = (MODE == MODE_IT) ? fpl + (size_t)(r0 + j) * A.f_rp : nullptr;
+      T rhs[GMAX][QW];
+#pragma unroll
+      for (int gi = 0; gi < GMAX; ++gi) {
+        const int gg = tid + gi * nthr;
+        if (gg < ng) {
+          const int x0 = gg * QW;
+          T uc[QW], ud[QW];
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const int x = x0 + q;
+            uc[q] = x < W ? L.get(i, x) : T(0);
+            ud[q] = x < W ? L.get(i + 1, x) : T(0);
+          }
+          T mxp = aux(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const int x = x0 + q;
+            if (x < W) {
+              const T ur = (q + 1 < QW && x + 1 < W) ? uc[q + 1] : L.get(i, wrapi(x + 1, W));
+              const T gx = ur - uc[q];
+              const T gy = ud[q] - uc[q];
+              const T mxq = aux(gx, P);
+              const T myq = aux(gy, P);
+              const T a = (mxp - mxq) + (myup[gi][q] - myq);
+              const T fv = (MODE == MODE_F0) ? uc[q] : frow[x];
+              rhs[gi][q] = fv + P.lam2 * a;
+              if (trace) {
+                const T d = uc[q] - fv;
+                e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
+              }
+              myup[gi][q] = myq;
+              mxp = mxq;
+            }
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int gi = 0; gi < GMAX; ++gi) {
+        const int gg = tid + gi * nthr;
+        if (gg < ng) {
+#pragma unroll
+          for (int q = 0; q < QW; ++q) {
+            const int x = gg * QW + q;
+            if (x < W) L.set(j, x, rhs[gi][q]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (trace) {
+      const double s = block_sum(e, red);
+      if (tid == 0) A.epart[(size_t)b * gridDim.x + blockIdx.x] = s;
+    }
+  }
+
+  // ---------------- phase C: r2c of rhs rows -> S_out (group per line)
+  for (int i = g.id; i < nb; i += ngroups) {
+    cx<T>* z = L.line(i);
+    fft_line<T, -1, FS>(z, A.fft, g);
+    if (PACKED) r2c_post<T>(z, A.N, A.wreal, g);
+    cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
+    for (int k = g.rank; k < A.Wc; k += g.size) dst[k] = z[pad<T>(k)];
+  }
+}
+
+// ------------------------------------------------------------ column pass
+// A strip of C columns is loaded transposed into C padded lines (line pitch
+// LPc chosen so the transposing load/store is bank-conflict-free); a group
+// owns one column at a time: forward FFT, * 1/(H W denom), inverse FFT.
+template <typename T, class FS>
+__global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const Group g{tid / A.fft.G, A.fft.G, tid % A.fft.G};
+  const int ngroups = nthr / A.fft.G;
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * A.C;
+  const int nc = min(A.C, A.Wc - c0);
+  const int H = A.H;
+  cx<T>* Spl = A.S + (size_t)b * A.S_ps + c0;
+  for (int t = tid; t < H * nc; t += nthr) {
+    const int y = t / nc, c = t - y * nc;
+    tile[c * A.CS + pad<T>(y)] = Spl[(size_t)y * A.S_rp + c];
+  }
+  __syncthreads();
+  for (int c = g.id; c < nc; c += ngroups) {
+    cx<T>* z = tile + c * A.CS;
+    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g);
+    if (A.mode == COL_SOLVE) {
+      // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses
+      const T wxc = __ldg(A.wx + c0 + c);
+      for (int y = g.rank; y < H; y += g.size) {
+        const T d = T(1) + A.cl2 * (__ldg(A.wy + y) + wxc);
+        z[pad<T>(y)] = scale(z[pad<T>(y)], A.inv_hw / d);
+      }
+      g.sync();
+    } else if (A.mode == COL_INV) {
+      for (int y = g.rank; y < H; y += g.size) z[pad<T>(y)] = scale(z[pad<T>(y)], A.inv_hw);
+      g.sync();
+    }
+    if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g);
+  }
+  __syncthreads();
+  for (int t = tid; t < H * nc; t += nthr) {
+    const int y = t / nc, c = t - y * nc;
+    Spl[(size_t)y * A.S_rp + c] = tile[c * A.CS + pad<T>(y)];
+  }
+}
+
+// ------------------------------------------------------------ small kernels
+// energies[b] = sum of partials in fixed order (deterministic)
+static __global__ void k_energy_reduce(const double* __restrict__ part, int nparts, int B, double* __restrict__ out) {
+  const int b = blockIdx.x;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[(size_t)b * nparts + i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[b] = s;
+}
+
+// BT.601 (image.py:110-128): planes [frame][3][H*W] in place
+template <typename T>
+__global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long npx, int nframes, int inverse) {
+  const long long n = npx * nframes;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long fr = t / npx, i = t - fr * npx;
+    T* q = p + fr * 3 * plane_stride + i;
+    const T a = q[0], b = q[plane_stride], c = q[2 * plane_stride];
+    if (!inverse) {
+      const T y = T(0.299) * a + T(0.587) * b + T(0.114) * c;
+      q[0] = y;
+      q[plane_stride] = T(0.492) * (c - y);
+      q[2 * plane_stride] = T(0.877) * (a - y);
+    } else {
+      const T r = a + c / T(0.877);
+      const T bb = a + b / T(0.492);
+      q[0] = r;
+      q[plane_stride] = (a - T(0.299) * r - T(0.114) * bb) / T(0.587);
+      q[2 * plane_stride] = bb;
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers
+// Compile-time FFT plans for the hot sizes (fp32).  Everything else runs the
+// runtime-planned path (FftRt).  The host planner (ils_api.cu) uses exactly
+// these radix lists when n matches, so twiddle tables and kernels agree.
+#define ILS_ROW_SPECS(X) X(0, 256, 16, 16) X(1, 960, 16, 15, 4) X(2, 1920, 16, 15, 8) X(3, 3840, 16, 16, 15) X(4, 512, 16, 8, 4)
+// row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
+#define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)
+#define ILS_COL_SPECS(X) X(0, 512, 16, 8, 4) X(1, 1080, 15, 9, 8) X(2, 2160, 16, 15, 9) X(3, 4320, 16, 15, 9, 2) X(4, 256, 16, 16)
+
+template <int ID>
+struct RowSpec;
+template <int ID>
+struct ColSpec;
+#define ILS_DEF_ROW_SPEC(ID, ...) \
+  template <>                     \
+  struct RowSpec<ID> {            \
+    using type = FftCt<__VA_ARGS__>; \
+  };
+#define ILS_DEF_COL_SPEC(ID, ...) \
+  template <>                     \
+  struct ColSpec<ID> {            \
+    using type = FftCt<__VA_ARGS__>; \
+  };
+ILS_ROW_SPECS(ILS_DEF_ROW_SPEC)
+ILS_COL_SPECS(ILS_DEF_COL_SPEC)
+
+template <typename T, bool PACKED, class FS, bool WIDE = false>
+cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
+template <typename T, class FS>
+cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
+
+#ifdef ILS_DEFINE_LAUNCHERS
+template <typename T, bool PACKED, class FS, bool WIDE>
+cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  auto k = k_row<T, PACKED, FS, WIDE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+template <typename T, class FS>
+cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  auto k = k_col<T, FS>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+#endif
+
+}  // namespace ils

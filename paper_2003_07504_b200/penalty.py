@@ -1,0 +1,98 @@
+"""Penalty parameter objects of the drop-in (mirrors reference penalty.py:40-126).
+
+These carry the parameters (validated exactly as the reference does) and the
+closed-form min_curvature the smoother needs.  value/derivative/edge_stop are
+host-side scalar/array helpers kept for API parity; the smoothing path never
+calls them -- phi'(x) and mu = c x - phi'(x) are evaluated inside the fused
+CUDA row kernel (csrc/ils_kernels.cuh: dphi/aux).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+DEFAULT_EPS = 1e-4
+_CURVATURE_SLACK = 1e-12
+
+
+@dataclass(frozen=True)
+class Charbonnier:
+    """Generalized Charbonnier penalty (x^2 + eps)^(p/2) (penalty.py:47-75)."""
+
+    p: float = 0.8
+    eps: float = DEFAULT_EPS
+
+    def __post_init__(self):
+        if not (0.0 < self.p <= 1.0):
+            raise ValueError("p must be in (0,1]")
+        if not (self.eps > 0.0):
+            raise ValueError(f"eps must be positive, got {self.eps}")
+
+    def value(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        return (x * x + self.eps) ** (self.p / 2.0)
+
+    def derivative(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        return self.p * x * (x * x + self.eps) ** (self.p / 2.0 - 1.0)
+
+    def edge_stop(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        return (self.p / 2.0) * (x * x + self.eps) ** (self.p / 2.0 - 1.0)
+
+    @property
+    def min_curvature(self) -> float:
+        return self.p * self.eps ** (self.p / 2.0 - 1.0)
+
+
+@dataclass(frozen=True)
+class Welsch:
+    """Welsch penalty 2 g^2 (1 - exp(-x^2 / 2 g^2)) (penalty.py:78-105)."""
+
+    gamma: float
+
+    def __post_init__(self):
+        if not (self.gamma > 0.0):
+            raise ValueError(f"gamma must be positive, got {self.gamma}")
+
+    def value(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        g2 = self.gamma * self.gamma
+        return 2.0 * g2 * (1.0 - np.exp(-x * x / (2.0 * g2)))
+
+    def derivative(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        g2 = self.gamma * self.gamma
+        return 2.0 * x * np.exp(-x * x / (2.0 * g2))
+
+    def edge_stop(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        g2 = self.gamma * self.gamma
+        return np.exp(-x * x / (2.0 * g2))
+
+    @property
+    def min_curvature(self) -> float:
+        return 2.0
+
+
+def check_curvature(spec, c: float) -> None:
+    """penalty.py:108-114."""
+    c0 = spec.min_curvature
+    if not np.isfinite(c) or c < c0 * (1.0 - _CURVATURE_SLACK):
+        raise ValueError(
+            f"curvature c={c} is below the minimum {c0} required for a "
+            f"convex bound with {type(spec).__name__}"
+        )
+
+
+def to_c_params(spec, lam: float, c: float, iters: int):
+    """Flatten (penalty, lam, c, iters) into the C ABI's ils_params."""
+    from ._lib import ILS_CHARBONNIER, ILS_WELSCH, Params
+
+    if isinstance(spec, Charbonnier):
+        return Params(ILS_CHARBONNIER, spec.p, spec.eps, 0.0, float(lam), float(c), int(iters))
+    if isinstance(spec, Welsch):
+        return Params(ILS_WELSCH, 0.0, 0.0, spec.gamma, float(lam), float(c), int(iters))
+    raise ValueError(f"unsupported penalty {type(spec).__name__}: the CUDA path implements Charbonnier and Welsch")

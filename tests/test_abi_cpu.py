@@ -1,0 +1,174 @@
+"""CPU-only checks of the C ABI boundary and host logic (no kernels launched)."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2003_07504_b200 as ils
+from paper_2003_07504_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "ils_b200.h")).read()
+    return sorted(set(re.findall(r"ILS_API\s+[\w\s\*]+?\b(ils_\w+)\s*\(", txt)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    L = _lib.lib()
+    syms = _header_symbols()
+    assert len(syms) == 14
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+    assert L.ils_abi_version() == 1
+
+
+def test_library_is_built_for_sm_100a():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def _host_plan(b, h, w, params, dtype=_lib.ILS_F32):
+    L = _lib.lib()
+    p = C.c_void_p()
+    st = L.ils_plan_create(C.byref(p), b, h, w, C.byref(params), dtype, -1)
+    return st, p
+
+
+@pytest.mark.parametrize("shape", [(1080, 1920), (512, 512), (17, 13), (5, 7), (2160, 3840), (1, 6), (3, 1),
+                                   (33, 45), (720, 1280), (59, 118)])
+@pytest.mark.parametrize("dtype", [_lib.ILS_F32, _lib.ILS_F64])
+def test_host_planner_radix_products(shape, dtype):
+    h, w = shape
+    prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
+    st, p = _host_plan(3, h, w, prm, dtype)
+    assert st == 0, _lib.last_error()
+    info = _lib.PlanInfo()
+    assert _lib.lib().ils_plan_get_info(p, C.byref(info)) == 0
+    d = info.as_dict()
+    n_row = w // 2 if w % 2 == 0 else w
+    assert int(np.prod(d["row_radix"] or [1])) == n_row
+    assert int(np.prod(d["col_radix"] or [1])) == h
+    assert all(r <= 61 for r in d["row_radix"] + d["col_radix"])
+    assert d["row_smem"] <= 227 * 1024 and d["col_smem"] <= 227 * 1024
+    assert d["spec_pitch"] >= w // 2 + 1
+    assert d["launches_per_call"] == 2 * 4 + 1
+    ws = C.c_size_t()
+    assert _lib.lib().ils_workspace_size(p, C.byref(ws)) == 0
+    assert ws.value >= 2 * 3 * h * (w // 2 + 1) * (8 if dtype == _lib.ILS_F32 else 16)
+    _lib.lib().ils_plan_destroy(p)
+
+
+def test_hot_sizes_use_compile_time_plans():
+    prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
+    st, p = _host_plan(3, 1080, 1920, prm)
+    info = _lib.PlanInfo()
+    _lib.lib().ils_plan_get_info(p, C.byref(info))
+    assert info.row_spec >= 0 and info.col_spec >= 0
+    _lib.lib().ils_plan_destroy(p)
+
+
+def test_unsupported_prime_and_bad_params_map_to_valueerror():
+    prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
+    st, _ = _host_plan(1, 1031, 64, prm)
+    assert st == _lib.ILS_EUNSUPPORTED
+    with pytest.raises(ValueError, match="prime factor"):
+        _lib.check(st)
+    bad = _lib.Params(_lib.ILS_CHARBONNIER, 1.5, 1e-4, 0.0, 1.0, 300.0, 4)
+    st, _ = _host_plan(1, 8, 8, bad)
+    assert st == _lib.ILS_EINVAL
+    with pytest.raises(ValueError, match=r"p must be in \(0,1\]"):
+        _lib.check(st)
+    low_c = _lib.Params(_lib.ILS_WELSCH, 0.0, 0.0, 0.1, 1.0, 1.0, 4)
+    assert _host_plan(1, 8, 8, low_c)[0] == _lib.ILS_EINVAL
+    zero_iters = _lib.Params(_lib.ILS_WELSCH, 0.0, 0.0, 0.1, 1.0, 2.0, 0)
+    assert _host_plan(1, 8, 8, zero_iters)[0] == _lib.ILS_EINVAL
+
+
+def test_host_only_plan_refuses_to_run():
+    prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
+    st, p = _host_plan(1, 8, 8, prm)
+    buf = (C.c_char * 4096)()
+    st = _lib.lib().ils_smooth(p, buf, buf, 64, buf, None, buf, None)
+    assert st == _lib.ILS_EINVAL
+    _lib.lib().ils_plan_destroy(p)
+
+
+def test_status_mapping():
+    with pytest.raises(ils.NumericalError):
+        _lib.check(_lib.ILS_ENONFINITE)
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.ILS_ECUDA)
+    _lib.check(_lib.ILS_OK)
+
+
+def test_params_validation_mirrors_reference():
+    # pkg/tests/test_smoother.py:42-57 and test_penalty.py:93-103
+    pen = ils.Charbonnier(0.8, 1e-4)
+    for kw in (dict(lam=0.0), dict(lam=-2.0), dict(lam=1.0, iters=0), dict(lam=1.0, c=pen.min_curvature / 2),
+               dict(lam=1.0, color_mode="rgb")):
+        with pytest.raises(ValueError):
+            ils.SmoothParams(pen, **kw)
+    with pytest.raises(ValueError, match=r"p must be in \(0,1\]"):
+        ils.Charbonnier(1.2)
+    with pytest.raises(ValueError):
+        ils.Welsch(0.0)
+    assert ils.SmoothParams(pen, 1.0).curvature == pen.min_curvature
+    assert ils.Charbonnier(0.8, 1e-4).min_curvature == pytest.approx(200.95091452076636, rel=1e-14)
+    for args in ((0, 4, 1.0, 2.0), (4, 4, -1.0, 2.0), (4, 4, 1.0, 0.0)):
+        with pytest.raises(ValueError):
+            ils.make_plan(*args)
+    with pytest.raises(ValueError):
+        ils.make_plan(4, 4, 1.0, 2.0, workers=0)
+    with pytest.raises(ValueError):
+        ils.make_plan(4, 4, 1.0, 2.0).with_data(np.zeros((5, 5)))
+
+
+def test_as_plane_and_multiimage_validation():
+    with pytest.raises(ValueError):
+        ils.as_plane(np.zeros(3))
+    with pytest.raises(ValueError):
+        ils.as_plane(np.zeros((0, 3)))
+    with pytest.raises(ValueError):
+        ils.as_plane(np.array([[np.nan]]))
+    with pytest.raises(ValueError):
+        ils.MultiImage((np.zeros((2, 2)),), ils.RGB)
+    img = ils.MultiImage.from_array(np.zeros((4, 5, 3)))
+    assert img.height == 4 and img.width == 5 and img.space == ils.RGB
+    assert not img.channels[0].flags.writeable
+
+
+def test_energy_trace_contract():
+    tr = ils.EnergyTrace([10.0, 6.0, 5.0, 4.0])
+    assert tr.rel_decrease(1) == pytest.approx(4.0 / 6.0)
+    assert tr.rel_decrease(3) == 1.0
+    with pytest.raises(ValueError):
+        tr.rel_decrease(4)
+    with pytest.raises(ValueError):
+        ils.EnergyTrace([]).rel_decrease(0)
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2003_07504_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith(".py"):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", txt), fn
+
+
+def test_no_cpu_fallback_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        ils.smooth_plane(np.zeros((8, 8)), ils.SmoothParams(ils.Charbonnier(0.8), 1.0))
