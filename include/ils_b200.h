@@ -132,6 +132,7 @@ typedef struct {
   int32_t row_passes, col_passes;
   int32_t row_group, col_group; /* threads per FFT line group */
   int32_t row_spec, col_spec;   /* compile-time FFT plan id, -1 = runtime plan */
+  int32_t row_swz, col_swz;     /* 1 = XOR-swizzled shared-memory line layout */
   int32_t row_radix[16];
   int32_t col_radix[16];
   int64_t spec_pitch;        /* complex elements per spectrum row */

@@ -39,7 +39,7 @@ class PlanInfo(C.Structure):
         "batch", "height", "width", "dtype", "packed",
         "row_band", "row_threads", "row_grid", "row_smem",
         "col_cols", "col_threads", "col_grid", "col_smem",
-        "row_passes", "col_passes", "row_group", "col_group", "row_spec", "col_spec")] + [
+        "row_passes", "col_passes", "row_group", "col_group", "row_spec", "col_spec", "row_swz", "col_swz")] + [
         ("row_radix", C.c_int32 * 16), ("col_radix", C.c_int32 * 16),
         ("spec_pitch", C.c_int64), ("launches_per_call", C.c_int32)]
 

@@ -59,6 +59,7 @@ bool pass_fits(int R, long long n, int G, int maxe) {
 struct FftHost {
   int n = 1;
   int G = 32;
+  int swz = 0;  // 1: XOR-swizzled line layout
   std::vector<int> radix;
   std::vector<int> tw_off, gen_off;
   std::vector<double> tw;  // interleaved re/im
@@ -109,42 +110,93 @@ bool has_big_prime(int n) {
 }
 
 struct SpecHost {
-  int id, n;
+  int id, swz, G, n;
   std::vector<int> radix;
 };
-#define ILS_HOST_SPEC(ID, N, ...) SpecHost{ID, N, {__VA_ARGS__}},
+#define ILS_HOST_SPEC(ID, SWZ, GG, N, ...) SpecHost{ID, SWZ, GG, N, {__VA_ARGS__}},
 const SpecHost kRowSpecs[] = {ILS_ROW_SPECS(ILS_HOST_SPEC)};
 const SpecHost kColSpecs[] = {ILS_COL_SPECS(ILS_HOST_SPEC)};
 #undef ILS_HOST_SPEC
 
+// Shared-memory wavefronts of one transform relative to the conflict-free
+// ideal, for a line layout (identity or XOR swizzle), following exactly the
+// index pattern of fft_pass.  E = complex elements per 128 B (16 fp32, 8 fp64);
+// a warp's request is served in phases of E lanes.
+double bank_cost(int n, const std::vector<int>& radix, int G, bool swz, int E, int maxe) {
+  const int sh = E == 16 ? 4 : 3;
+  auto lay = [&](int e) { return swz ? (e ^ ((e >> sh) & (E - 1))) : e; };
+  auto wave = [&](const int* addr, const bool* act, int lanes, double& tot, double& ideal) {
+    for (int p0 = 0; p0 < lanes; p0 += E) {
+      int cnt[16] = {0};
+      int seen[32];
+      int ns = 0;
+      bool any = false;
+      for (int l = p0; l < p0 + E && l < lanes; ++l) {
+        if (!act[l]) continue;
+        any = true;
+        bool dup = false;
+        for (int q = 0; q < ns; ++q) dup = dup || seen[q] == addr[l];
+        if (dup) continue;
+        seen[ns++] = addr[l];
+        cnt[addr[l] % E]++;
+      }
+      if (!any) continue;
+      ideal += 1;
+      tot += *std::max_element(cnt, cnt + E);
+    }
+  };
+  double tot = 0, ideal = 0;
+  int Ns = 1;
+  for (int R : radix) {
+    const int nb = n / R, km = R <= 16 ? std::max(1, maxe / R) : 1;
+    for (int k = 0; k < km; ++k)
+      for (int w0 = 0; w0 < G; w0 += 32) {
+        int ld[32], st[32];
+        bool act[32];
+        for (int r = 0; r < R; ++r) {
+          for (int l = 0; l < 32; ++l) {
+            const int j = w0 + l + k * G;
+            act[l] = j < nb;
+            ld[l] = lay(j + r * nb);
+            st[l] = lay((j - j % Ns) * R + j % Ns + r * Ns);
+          }
+          wave(ld, act, 32, tot, ideal);
+          wave(st, act, 32, tot, ideal);
+        }
+      }
+    Ns *= R;
+  }
+  return ideal > 0 ? tot / ideal : 1.0;
+}
+
 // Radix plan + twiddles for an n-point line transform.  A compile-time spec
-// (fp32 hot sizes) fixes the radices; otherwise the plan with fewest passes.
-// G is the smallest group size (32..256) for which every pass fits.
-bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec) {
+// (fp32 hot sizes) fixes radices, group size and layout; otherwise the plan
+// with fewest passes at the smallest group size G (32..256) for which every
+// pass fits, and the layout with fewer simulated bank conflicts.
+bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
   out = FftHost{};
   out.n = n;
-  bool ok = n <= 1;
-  for (int G = 32; G <= 256 && !ok; G *= 2) {
-    if (spec) {
-      bool fits = true;
-      for (int R : spec->radix) fits = fits && pass_fits(R, n, G, maxe);
-      if (fits) {
-        out.radix = spec->radix;
+  if (spec) {
+    for (int R : spec->radix)
+      if (!pass_fits(R, n, spec->G, maxe)) return false;
+    out.radix = spec->radix;
+    out.G = spec->G;
+    out.swz = spec->swz;
+  } else {
+    bool ok = n <= 1;
+    for (int G = 32; G <= 256 && !ok; G *= 2) {
+      std::vector<int> cur, best;
+      bool found = false;
+      dfs(n, 1 << 30, n, G, maxe, cur, best, found);
+      if (found) {
+        out.radix = best;
         out.G = G;
         ok = true;
       }
-      continue;
     }
-    std::vector<int> cur, best;
-    bool found = false;
-    dfs(n, 1 << 30, n, G, maxe, cur, best, found);
-    if (found) {
-      out.radix = best;
-      out.G = G;
-      ok = true;
-    }
+    if (!ok) return false;
+    out.swz = bank_cost(n, out.radix, out.G, true, E, maxe) < bank_cost(n, out.radix, out.G, false, E, maxe);
   }
-  if (!ok) return false;
   if ((int)out.radix.size() > kMaxPass) return false;
   long long Ns = 1;
   for (int R : out.radix) {
@@ -180,6 +232,7 @@ struct ils_plan {
   int C, CS, col_threads, col_grid;
   size_t col_smem;
   int row_spec = -1, col_spec = -1;  // compile-time FFT plan ids (-1: runtime plan)
+  int sms = 148;                     // SMs of the plan's device (waves model)
   FftHost rowf, colf;
   void* d_tables = nullptr;
   size_t off_rowtw, off_coltw, off_wreal, off_wx, off_wy, off_sink;  // byte offsets
@@ -194,10 +247,6 @@ size_t esz() {
   return sizeof(cx<T>);
 }
 
-int padded_len_rt(int n, size_t elt) {
-  return elt == 8 ? padded_len<float>(n) : padded_len<double>(n);
-}
-
 template <size_t K>
 const SpecHost* find_spec(const SpecHost (&tab)[K], int n) {
   if (env_int("ILS_NO_SPECS", 0)) return nullptr;
@@ -209,55 +258,110 @@ const SpecHost* find_spec(const SpecHost (&tab)[K], int n) {
 bool choose_row(ils_plan& p, int maxe, size_t elt) {
   const SpecHost* spec = (p.dtype == ILS_F32 && p.packed) ? find_spec(kRowSpecs, p.N) : nullptr;
   p.row_spec = spec ? spec->id : -1;
-  if (!make_fft(p.N, maxe, p.rowf, spec)) return false;
+  if (!make_fft(p.N, maxe, p.rowf, spec, elt == 8 ? 16 : 8)) {
+    if (!spec || !make_fft(p.N, maxe, p.rowf, nullptr, elt == 8 ? 16 : 8)) return false;
+    p.row_spec = -1;
+  }
   if (p.W > kWideMaxW || (p.W > kNarrowMaxW && !p.packed)) return false;  // stencil strip registers
   const int line = p.packed ? p.N + 1 : p.N;
-  const int LP = (padded_len_rt(line, elt) + 1) & ~1;
-  const size_t budget = (size_t)env_int("ILS_SMEM_BUDGET", 110 * 1024);
-  int band = std::min(p.H, env_int("ILS_ROW_BAND", 16));
-  // wide rows: take the whole shared memory rather than a 1-row band
-  const size_t bud = (size_t)LP * elt * 6 > budget ? std::max(budget, (size_t)227 * 1024) : budget;
-  while (band > 1 && (size_t)(band + 2) * LP * elt > bud) --band;
-  if ((size_t)(band + 2) * LP * elt > 227 * 1024) return false;
-  p.band = band;
+  // a swizzled layout permutes inside whole 128-byte blocks: round up to them
+  const int E = elt == 8 ? 16 : 8;
+  const int LP = p.rowf.swz ? (line + E - 1) / E * E : (line + 1) & ~1;
+  // Band size: minimise (waves x per-CTA work).  A CTA of band b transforms
+  // b+2 lines c2r and b lines r2c; 2 CTAs fit an SM while smem <= ~113 KB.
+  const int force = env_int("ILS_ROW_BAND", 0);
+  double best = 1e300;
+  for (int band = 1; band <= std::min(p.H, 24); ++band) {
+    if (force && band != std::min(force, p.H)) continue;
+    const size_t smem = (size_t)(band + 2) * LP * elt;
+    if (smem > 227 * 1024) break;
+    const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+    const long ctas = (long)p.B * ((p.H + band - 1) / band);
+    const long slots = (long)p.sms * per_sm;
+    const double waves = (double)((ctas + slots - 1) / slots);
+    const double cost = waves * (2.0 * band + 2.0 + 0.5 * band) * (per_sm == 1 ? 2.0 : 1.0);
+    if (cost < best * (1 - 1e-9)) {
+      best = cost;
+      p.band = band;
+      p.row_smem = smem;
+    }
+  }
+  if (best == 1e300) return false;
   p.row_threads = kRowThreads;
   p.LP = LP;
-  p.row_smem = (size_t)(band + 2) * LP * elt;
-  p.row_grid = (p.H + band - 1) / band;
+  p.row_grid = (p.H + p.band - 1) / p.band;
   return true;
 }
 
 bool choose_col(ils_plan& p, int maxe, size_t elt) {
   const SpecHost* spec = p.dtype == ILS_F32 ? find_spec(kColSpecs, p.H) : nullptr;
   p.col_spec = spec ? spec->id : -1;
-  if (!make_fft(p.H, maxe, p.colf, spec)) return false;
-  const size_t budget = (size_t)env_int("ILS_SMEM_BUDGET", 110 * 1024);
+  if (!make_fft(p.H, maxe, p.colf, spec, elt == 8 ? 16 : 8)) {
+    if (!spec || !make_fft(p.H, maxe, p.colf, nullptr, elt == 8 ? 16 : 8)) return false;
+    p.col_spec = -1;
+  }
   const int E = elt == 8 ? 16 : 8;  // complex elements per 128 B
-  const int fc = env_int("ILS_COL_COLS", 0);
-  const int opts[] = {8, 4, 16, 2, 1};
-  for (int C : opts) {
-    if (fc) C = fc;
-    const int Cu = std::min(C, p.Wc);
-    const int base = (padded_len_rt(p.H, elt) + E - 1) / E * E;
-    const int CS = base + ((32 / std::max(Cu, 1)) % E);
-    const size_t smem = (size_t)Cu * CS * elt;
-    if (smem <= budget || C == 1 || fc) {
-      if (smem > 227 * 1024) return false;
-      p.C = Cu;
-      p.CS = CS;
-      p.col_threads = kColThreads;
+  const int ngroups = kColThreads / p.colf.G;
+  const int force = env_int("ILS_COL_COLS", 0);
+  const int base = (p.H + E - 1) / E * E;
+  double best = 1e300;
+  for (int C = 1; C <= std::min(p.Wc, 32); ++C) {
+    if (force && C != std::min(force, p.Wc)) continue;
+    // line pitch: pick the offset whose transposing copy has fewest conflicts
+    int bestCS = base;
+    int bestw = 1 << 30;
+    for (int o = 0; o < E; ++o) {
+      const int CS = base + o;
+      int tot = 0;
+      for (int t0 = 0; t0 < 64; t0 += E) {
+        int cnt[16] = {0};
+        for (int t = t0; t < t0 + E; ++t) {
+          const int y = t / C, c = t % C;
+          const int e = c * CS + (p.colf.swz ? (y ^ ((y >> (E == 16 ? 4 : 3)) & (E - 1))) : y);
+          cnt[e % E]++;
+        }
+        tot += *std::max_element(cnt, cnt + E);
+      }
+      if (tot < bestw) {
+        bestw = tot;
+        bestCS = CS;
+      }
+    }
+    const size_t smem = (size_t)C * bestCS * elt;
+    if (smem > 227 * 1024) break;
+    const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+    const long strips = (p.Wc + C - 1) / C;
+    const long ctas = (long)p.B * strips;
+    const long slots = (long)p.sms * per_sm;
+    const double waves = (double)((ctas + slots - 1) / slots);
+    // 32-byte sectors a strip's row segment touches (rows are 32 B aligned)
+    double sectors = 0;
+    for (long s = 0; s < strips; ++s) {
+      const long b0 = s * C * (long)elt, b1 = std::min<long>((s + 1) * C, p.Wc) * (long)elt;
+      sectors += (double)((b1 + 31) / 32 - b0 / 32);
+    }
+    sectors /= strips;
+    const double col_sectors = (double)elt / 32.0;  // one column's share at perfect coalescing
+    const double cost =
+        waves * ((C + ngroups - 1) / ngroups + 0.5 * sectors / col_sectors) * (per_sm == 1 ? 2.0 : 1.0);
+    if (cost < best * (1 - 1e-6) || (cost < best * (1 + 1e-6) && C > p.C)) {
+      best = cost;
+      p.C = C;
+      p.CS = bestCS;
       p.col_smem = smem;
-      p.col_grid = (p.Wc + Cu - 1) / Cu;
-      return true;
     }
   }
-  return false;
+  if (best == 1e300) return false;
+  p.col_threads = kColThreads;
+  p.col_grid = (p.Wc + p.C - 1) / p.C;
+  return true;
 }
 
 template <typename T>
 void fill_fft_dev(FftDev<T>& d, const FftHost& h, const void* base, size_t off) {
   d.n = h.n;
   d.G = h.G;
+  d.laymask = h.swz ? (sizeof(T) == 4 ? 15 : 7) : 0;
   d.npass = (int)h.radix.size();
   for (int i = 0; i < kMaxPass; ++i) {
     d.radix[i] = i < d.npass ? h.radix[i] : 1;
@@ -473,12 +577,16 @@ ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_
   p->packed = (width % 2 == 0);
   p->N = p->packed ? width / 2 : width;
   p->Wc = width / 2 + 1;
-  p->Sp = (p->Wc + 1) & ~1;
+  p->Sp = (p->Wc + 3) & ~3;  // 32-byte aligned spectrum rows (fp32)
   p->dtype = dtype;
   p->device = device;
   p->prm = *params;
   const size_t elt = dtype == ILS_F32 ? sizeof(cx<float>) : sizeof(cx<double>);
   const int maxe = dtype == ILS_F32 ? 16 : 8;
+  if (device >= 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) p->sms = sms;
+  }
   if (!choose_row(*p, maxe, elt) || !choose_col(*p, maxe, elt)) {
     delete p;
     return fail(ILS_EUNSUPPORTED, "no launch configuration fits plane size %dx%d", height, width);
@@ -571,6 +679,8 @@ ils_status ils_plan_get_info(const ils_plan* p, ils_plan_info* i) {
   i->col_group = p->colf.G;
   i->row_spec = p->row_spec;
   i->col_spec = p->col_spec;
+  i->row_swz = p->rowf.swz;
+  i->col_swz = p->colf.swz;
   i->row_grid = p->row_grid;
   i->row_smem = (int32_t)p->row_smem;
   i->col_cols = p->C;

@@ -13,8 +13,14 @@
 // A thread holds KM = MAXE/R butterflies in registers across the group
 // barrier, so the pass runs in place and the output is in natural order.
 // Register need depends on n/G only, never on how many lines a CTA holds.
-// Element e of a line lives at pad(e) = e + (e >> PADSH): one spare slot per
-// 128 bytes, which makes the stride-R stores of early passes conflict-free.
+//
+// Shared-memory layout: element e of a line lives at slot L(e), where L is
+// either the identity or an XOR swizzle of e's position inside its 128-byte
+// block by e's block index (L(e) = e ^ ((e >> SH) & MASK)).  Which one is
+// cheaper depends on the radix plan (stride-R stores of even radices
+// conflict without it; radix-15 first passes conflict with it); the host
+// planner simulates the bank traffic of both and picks per plan.
+//
 // Twiddles come from a per-pass table [m][r-1] computed on the host in double
 // with exact integer angle reduction.  Radices 2..16 are unrolled; odd primes
 // 17..61 use a looped direct DFT (generic sizes only).
@@ -31,26 +37,32 @@ template <typename T>
 struct FftDev {
   int n;
   int npass;
-  int G;  // threads per line group
+  int G;        // threads per line group
+  int laymask;  // swizzle mask of the line layout (0 = identity)
   int radix[kMaxPass];
   int tw_off[kMaxPass];   // pass twiddles: Ns*(R-1) entries, layout [m][r-1]
   int gen_off[kMaxPass];  // generic primes: R entries w_R^q
   const cx<T>* tw;
 };
 
+// complex elements per 128 bytes = 1 << SwzShift<T>
 template <typename T>
-struct PadOf {
-  static constexpr int SH = sizeof(T) == 4 ? 4 : 3;  // 16 x 8 B or 8 x 16 B per 128 B
+struct SwzShift {
+  static constexpr int value = sizeof(T) == 4 ? 4 : 3;
 };
 template <typename T>
-__host__ __device__ __forceinline__ constexpr int pad(int e) {
-  return e + (e >> PadOf<T>::SH);
-}
-// complex slots a padded line of n elements occupies
+constexpr int kSwzMask = (1 << SwzShift<T>::value) - 1;
+
+// Line layouts.  LayoutCt: compile-time mask (hot sizes); LayoutRt: runtime.
+template <typename T, int MASK>
+struct LayoutCt {
+  __device__ __forceinline__ int operator()(int e) const { return e ^ ((e >> SwzShift<T>::value) & MASK); }
+};
 template <typename T>
-__host__ __device__ constexpr int padded_len(int n) {
-  return n > 0 ? pad<T>(n - 1) + 1 : 1;
-}
+struct LayoutRt {
+  int mask;
+  __device__ __forceinline__ int operator()(int e) const { return e ^ ((e >> SwzShift<T>::value) & mask); }
+};
 
 template <typename T>
 struct MaxElems {
@@ -61,13 +73,16 @@ struct KmOf {
   static constexpr int value = (MAXE / R) > 0 ? (MAXE / R) : 1;
 };
 
-struct Group {
-  int id;    // group index inside the CTA (named barrier id + 1)
-  int size;  // threads in the group (multiple of 32)
-  int rank;  // thread index inside the group
+// Group of G threads owning one line.  GC > 0 makes the size compile-time.
+template <int GC>
+struct GroupT {
+  int id;     // group index inside the CTA (named barrier id - 1)
+  int size_;  // runtime size (GC == 0)
+  int rank;   // thread index inside the group
+  __device__ __forceinline__ int size() const { return GC > 0 ? GC : size_; }
   __device__ __forceinline__ void sync() const {
-    if (size == 32) __syncwarp();
-    else asm volatile("bar.sync %0, %1;" ::"r"(id + 1), "r"(size) : "memory");
+    if (size() == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(id + 1), "r"(size()) : "memory");
   }
 };
 
@@ -82,9 +97,8 @@ __device__ __forceinline__ cx<T> ldg_cx(const cx<T>* p) {
   }
 }
 
-// Twiddle load pinned between the pass barriers: a plain __ldg of read-only
-// data may be hoisted by the compiler above every barrier of the whole
-// transform, which keeps all passes' twiddles live at once.
+// Twiddle load pinned between the pass barriers (a plain __ldg of read-only
+// data may be hoisted above every barrier of the transform).
 template <typename T>
 __device__ __forceinline__ cx<T> ldtw(const cx<T>* p) {
   cx<T> v;
@@ -95,18 +109,29 @@ __device__ __forceinline__ cx<T> ldtw(const cx<T>* p) {
   return v;
 }
 
-template <typename T, int R, int KM, int DIR>
+// ---- asynchronous global -> shared copies (LDGSTS), no register staging
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <typename T, int R, int KM, int DIR, class Grp, class Lay>
 __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, const cx<T>* __restrict__ tw,
-                                         const Group& g) {
+                                         const Grp& g, const Lay& lay) {
   // Idle slots (j >= nb) recompute the last butterfly instead of skipping it:
   // conditionally-defined register arrays become loop-carried live ranges in
   // the caller's line loop and triple the register footprint.
   cx<T> v[KM][R];
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
-    const int j = min(g.rank + k * g.size, nb - 1);
+    const int j = min(g.rank + k * g.size(), nb - 1);
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[k][r] = x[pad<T>(j + r * nb)];
+    for (int r = 0; r < R; ++r) v[k][r] = x[lay(j + r * nb)];
     if (Ns > 1) {
       const cx<T>* w = tw + (j % Ns) * (R - 1);
 #pragma unroll
@@ -121,22 +146,22 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
   g.sync();
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
-    const int j = g.rank + k * g.size;
+    const int j = g.rank + k * g.size();
     if (j < nb) {
       const int m = j % Ns;
       const int base = (j - m) * R + m;
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[pad<T>(base + r * Ns)] = v[k][r];
+      for (int r = 0; r < R; ++r) x[lay(base + r * Ns)] = v[k][r];
     }
   }
   g.sync();
 }
 
 // Generic odd prime R (17..61): one butterfly per thread, looped direct DFT.
-template <typename T, int DIR>
+template <typename T, int DIR, class Grp, class Lay>
 __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int Ns, int R,
                                               const cx<T>* __restrict__ tw, const cx<T>* __restrict__ wr,
-                                              const Group& g) {
+                                              const Grp g, const Lay lay) {
   const int nb = n / R;
   cx<T> in[kMaxGenericPrime], out[kMaxGenericPrime];
   const int j = g.rank;
@@ -144,7 +169,7 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
   if (act) {
     const int m = j % Ns;
     for (int r = 0; r < R; ++r) {
-      cx<T> a = x[pad<T>(j + r * nb)];
+      cx<T> a = x[lay(j + r * nb)];
       if (Ns > 1 && r > 0) {
         cx<T> ww = ldg_cx(tw + m * (R - 1) + r - 1);
         if (DIR > 0) ww.y = -ww.y;
@@ -169,7 +194,7 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
   if (act) {
     const int m = j % Ns;
     const int base = (j - m) * R + m;
-    for (int r = 0; r < R; ++r) x[pad<T>(base + r * Ns)] = out[r];
+    for (int r = 0; r < R; ++r) x[lay(base + r * Ns)] = out[r];
   }
   g.sync();
 }
@@ -177,26 +202,24 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
 // Runtime-planned path (any supported n): each radix pass is its own
 // non-inlined function so the register allocator sees one radix at a time
 // (inlining all cases into one body blows up live ranges and spills).
-template <typename T, int R, int DIR>
+template <typename T, int R, int DIR, class Grp, class Lay>
 __device__ __noinline__ void fft_pass_rt(cx<T>* __restrict__ x, int nb, int Ns, const cx<T>* __restrict__ tw,
-                                         const Group g) {
-  fft_pass<T, R, KmOf<R, MaxElems<T>::value>::value, DIR>(x, nb, Ns, tw, g);
+                                         const Grp g, const Lay lay) {
+  fft_pass<T, R, KmOf<R, MaxElems<T>::value>::value, DIR>(x, nb, Ns, tw, g, lay);
 }
 
-// Full n-point transform of one padded line (DIR = -1 forward, +1 inverse,
-// unnormalised) from a runtime radix plan.  Every thread of the group must
-// call it.
-template <typename T, int DIR>
-__device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<T>& P, const Group& g) {
+template <typename T, int DIR, class Grp, class Lay>
+__device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
+                                            const Lay& lay) {
   int Ns = 1;
   for (int p = 0; p < P.npass; ++p) {
     const int R = P.radix[p];
     const int nb = P.n / R;
     const cx<T>* tw = P.tw + P.tw_off[p];
     switch (R) {
-#define ILS_FFT_CASE(RR)                                                  \
-  case RR:                                                                \
-    fft_pass_rt<T, RR, DIR>(x, nb, Ns, tw, g);                            \
+#define ILS_FFT_CASE(RR)                            \
+  case RR:                                          \
+    fft_pass_rt<T, RR, DIR>(x, nb, Ns, tw, g, lay); \
     break;
       ILS_FFT_CASE(2)
       ILS_FFT_CASE(3)
@@ -214,38 +237,54 @@ __device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<
       ILS_FFT_CASE(16)
 #undef ILS_FFT_CASE
       default:
-        fft_pass_generic<T, DIR>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g);
+        fft_pass_generic<T, DIR>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g, lay);
         break;
     }
     Ns *= R;
   }
 }
 
-// ------------------------------------------------------------ compile-time plans
-// The hot sizes get a compile-time radix list: straight-line passes with n,
-// Ns and every index constant-folded.  FftRt selects the runtime path.
+// ------------------------------------------------------------ plans as types
+// FftRt: runtime plan (FftDev), runtime group size and layout.
+// FftCt<SWZ, G, N, radices...>: the hot sizes -- group size, layout, n, Ns
+// and every index are compile-time constants.
 struct FftRt {
   static constexpr int n = 0;
+  static constexpr int G = 0;
+  template <typename T>
+  using Layout = LayoutRt<T>;
+  template <typename T>
+  __device__ static Layout<T> layout(const FftDev<T>& P) {
+    return Layout<T>{P.laymask};
+  }
 };
-template <int N, int... Rs>
+template <int SWZ, int GG, int N, int... Rs>
 struct FftCt {
   static constexpr int n = N;
+  static constexpr int G = GG;
+  static constexpr int swz = SWZ;
   static constexpr int npass = sizeof...(Rs);
   static_assert((Rs * ... * 1) == N, "radix product must equal N");
+  template <typename T>
+  using Layout = LayoutCt<T, SWZ ? kSwzMask<T> : 0>;
+  template <typename T>
+  __device__ static Layout<T> layout(const FftDev<T>&) {
+    return Layout<T>{};
+  }
 };
 
-template <typename T, int DIR, int N, int... Rs>
-__device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Group& g,
-                                            FftCt<N, Rs...>) {
+template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, class Lay>
+__device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Lay& lay,
+                                            FftCt<SWZ, GG, N, Rs...>) {
   constexpr int ME = MaxElems<T>::value;
   int Ns = 1, p = 0;
-  ((fft_pass<T, Rs, KmOf<Rs, ME>::value, DIR>(x, N / Rs, Ns, P.tw + P.tw_off[p], g), Ns *= Rs, ++p), ...);
+  ((fft_pass<T, Rs, KmOf<Rs, ME>::value, DIR>(x, N / Rs, Ns, P.tw + P.tw_off[p], g, lay), Ns *= Rs, ++p), ...);
 }
 
-template <typename T, int DIR, class S>
-__device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Group& g) {
-  if constexpr (S::n == 0) fft_line_rt<T, DIR>(x, P, g);
-  else fft_line_ct<T, DIR>(x, P, g, S{});
+template <typename T, int DIR, class S, class Grp, class Lay>
+__device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Lay& lay) {
+  if constexpr (S::n == 0) fft_line_rt<T, DIR>(x, P, g, lay);
+  else fft_line_ct<T, DIR>(x, P, g, lay, S{});
 }
 
 }  // namespace ils

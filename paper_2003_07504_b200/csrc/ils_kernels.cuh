@@ -113,20 +113,22 @@ template <typename T>
 __device__ __forceinline__ bool finite_(T v) { return isfinite(v); }
 
 // ------------------------------------------------------------ line access
-// Line i of a row CTA starts at lines + i*LP (complex slots, padded).  In a
-// packed line, real sample x lives in complex slot x>>1, component x&1.
-template <typename T, bool PACKED>
+// Line i of a row CTA starts at lines + i*LP (complex slots, layout Lay).
+// In a packed line, real sample x lives in complex element x>>1, component
+// x&1; element pairs (2q, 2q+1) stay adjacent under either layout.
+template <typename T, bool PACKED, class Lay>
 struct Lines {
   cx<T>* base;
   int LP;
+  Lay lay;
   __device__ __forceinline__ cx<T>* line(int i) const { return base + (size_t)i * LP; }
   __device__ __forceinline__ T get(int i, int x) const {
-    if (PACKED) return reinterpret_cast<const T*>(line(i))[2 * pad<T>(x >> 1) + (x & 1)];
-    return line(i)[pad<T>(x)].x;
+    if (PACKED) return reinterpret_cast<const T*>(line(i))[2 * lay(x >> 1) + (x & 1)];
+    return line(i)[lay(x)].x;
   }
   __device__ __forceinline__ void set(int i, int x, T v) const {
-    if (PACKED) reinterpret_cast<T*>(line(i))[2 * pad<T>(x >> 1) + (x & 1)] = v;
-    else line(i)[pad<T>(x)] = cx<T>{v, T(0)};
+    if (PACKED) reinterpret_cast<T*>(line(i))[2 * lay(x >> 1) + (x & 1)] = v;
+    else line(i)[lay(x)] = cx<T>{v, T(0)};
   }
 };
 
@@ -147,25 +149,40 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
+// Wait until at most `keep` of this thread's cp.async groups are pending.
+__device__ __forceinline__ void cp_async_wait_keep(int keep) {
+  switch (keep) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+  }
+}
+
 // ------------------------------------------------------------ real <-> half-complex packing
 // Forward post-process of one packed line: Z = FFT_N(x[2n] + i x[2n+1]) ->
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
-// O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to slot N.
-template <typename T>
-__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Group& g) {
-  for (int k = g.rank; k <= N / 2; k += g.size) {
+// O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
+template <typename T, class Grp, class Lay>
+__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g,
+                                         const Lay& lay) {
+  for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
-      const cx<T> z0 = z[0];
-      z[0] = cx<T>{z0.x + z0.y, T(0)};
-      z[pad<T>(N)] = cx<T>{z0.x - z0.y, T(0)};
+      const cx<T> z0 = z[lay(0)];
+      z[lay(0)] = cx<T>{z0.x + z0.y, T(0)};
+      z[lay(N)] = cx<T>{z0.x - z0.y, T(0)};
     } else {
-      const cx<T> zk = z[pad<T>(k)], zm = z[pad<T>(N - k)];
+      const cx<T> zk = z[lay(k)], zm = z[lay(N - k)];
       const cx<T> E{T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y)};
       const cx<T> d{T(0.5) * (zk.x - zm.x), T(0.5) * (zk.y + zm.y)};  // (zk - conj zm)/2
       const cx<T> O{d.y, -d.x};                                          // -i * d
       const cx<T> wO = cmul(ldg_cx(wreal + k), O);
-      z[pad<T>(k)] = E + wO;
-      if (N - k != k) z[pad<T>(N - k)] = conj(E - wO);
+      z[lay(k)] = E + wO;
+      if (N - k != k) z[lay(N - k)] = conj(E - wO);
     }
   }
   g.sync();
@@ -174,19 +191,20 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restric
 // Inverse pre-process: Z_k = E + iO, Z_{N-k} = conj(E) + i conj(O) with
 // E = X_k + conj X_{N-k}, O = (X_k - conj X_{N-k}) conj(w^k).  An inverse
 // N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
-template <typename T>
-__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Group& g) {
-  for (int k = g.rank; k <= N / 2; k += g.size) {
+template <typename T, class Grp, class Lay>
+__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g,
+                                        const Lay& lay) {
+  for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
-      const T a = z[0].x, c = z[pad<T>(N)].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
-      z[0] = cx<T>{a + c, a - c};
+      const T a = z[lay(0)].x, c = z[lay(N)].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
+      z[lay(0)] = cx<T>{a + c, a - c};
     } else {
-      const cx<T> xk = z[pad<T>(k)], xm = z[pad<T>(N - k)];
+      const cx<T> xk = z[lay(k)], xm = z[lay(N - k)];
       const cx<T> E{xk.x + xm.x, xk.y - xm.y};
       const cx<T> D{xk.x - xm.x, xk.y + xm.y};
       const cx<T> O = cmulc(D, ldg_cx(wreal + k));
-      z[pad<T>(k)] = cx<T>{E.x - O.y, E.y + O.x};
-      if (N - k != k) z[pad<T>(N - k)] = cx<T>{E.x + O.y, -E.y + O.x};
+      z[lay(k)] = cx<T>{E.x - O.y, E.y + O.x};
+      if (N - k != k) z[lay(N - k)] = cx<T>{E.x + O.y, -E.y + O.x};
     }
   }
   g.sync();
@@ -194,18 +212,21 @@ __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict
 
 // ------------------------------------------------------------ row pass
 constexpr int kRowThreads = 256;
+constexpr int kColThreads = 256;
 constexpr int kNarrowMaxW = 4 * 4 * kRowThreads;  // stencil: 4 strips x 4 columns per thread
 constexpr int kWideMaxW = 4 * 8 * kRowThreads;
-constexpr int kColThreads = 256;
 
 template <typename T, bool PACKED, class FS, bool WIDE>
 __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
+  using Grp = GroupT<FS::G>;
   const int MODE = A.mode;  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const Group g{tid / A.fft.G, A.fft.G, tid % A.fft.G};
-  const int ngroups = nthr / A.fft.G;
+  const int G = FS::G > 0 ? FS::G : A.fft.G;
+  const Grp g{tid / G, G, tid % G};
+  const int ngroups = nthr / G;
+  const auto lay = FS::template layout<T>(A.fft);
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * A.band;
   const int nb = min(A.band, A.H - r0);
@@ -215,7 +236,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   const int nl = halo ? nb + 2 : nb;
   const int y0 = halo ? r0 - 1 : r0;
   const int off = halo ? 1 : 0;
-  const Lines<T, PACKED> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP};
+  const Lines<T, PACKED, decltype(lay)> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP, lay};
   const PenaltyDev<T>& P = A.pen;
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
 
@@ -226,7 +247,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     const T* my = A.muy ? A.muy + (size_t)b * A.f_ps : nullptr;
     for (int i = g.id; i < nb; i += ngroups) {
       const int r = r0 + i;
-      for (int x = g.rank; x < W; x += g.size) {
+      for (int x = g.rank; x < W; x += g.size()) {
         const size_t o = (size_t)r * A.f_rp + x;
         T v = fpl[o];
         bf |= !finite_(v);
@@ -255,31 +276,52 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     }
   } else {
     // ---------------- phase A: u rows into shared memory (group per line)
+    // Every group first issues asynchronous copies for all of its lines (one
+    // cp.async group per line), then transforms them in order while later
+    // lines are still in flight.
+    const int mine = (nl - g.id + ngroups - 1) / ngroups;  // lines owned by this group
+    const bool async_in = (MODE != MODE_F0) || PACKED;
+    if (async_in) {
+      for (int i = g.id; i < nl; i += ngroups) {
+        const int y = wrapi(y0 + i, H);
+        cx<T>* z = L.line(i);
+        if (MODE == MODE_F0) {
+          const cx<T>* src = reinterpret_cast<const cx<T>*>(fpl + (size_t)y * A.f_rp);
+          for (int q = g.rank; q < W / 2; q += g.size()) cp_async<sizeof(cx<T>)>(z + lay(q), src + q);
+        } else {
+          const cx<T>* src = A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp;
+          for (int k = g.rank; k < A.Wc; k += g.size()) cp_async<sizeof(cx<T>)>(z + lay(k), src + k);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+    }
     bool bad = false;
-    for (int i = g.id; i < nl; i += ngroups) {
+    int li = 0;
+    for (int i = g.id; i < nl; i += ngroups, ++li) {
       const int y = wrapi(y0 + i, H);
       cx<T>* z = L.line(i);
-      if (MODE == MODE_F0) {
-        for (int x = g.rank; x < W; x += g.size) {
-          const T v = fpl[(size_t)y * A.f_rp + x];
-          if (i >= off && i < off + nb) bad |= !finite_(v);
-          L.set(i, x, v);
-        }
-      } else {
-        const cx<T>* src = A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp;
-        for (int k = g.rank; k < A.Wc; k += g.size) z[pad<T>(k)] = src[k];
+      const bool own = i >= off && i < off + nb;
+      if (async_in) {
+        cp_async_wait_keep(mine - 1 - li);
         g.sync();
+      }
+      if (MODE == MODE_F0) {
+        if (!PACKED)
+          for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
+        if (own)
+          for (int x = g.rank; x < W; x += g.size()) bad |= !finite_(L.get(i, x));
+      } else {
         if (PACKED) {
-          c2r_pre<T>(z, A.N, A.wreal, g);
+          c2r_pre<T>(z, A.N, A.wreal, g, lay);
         } else {
           // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
-          for (int k = A.Wc + g.rank; k < W; k += g.size) z[pad<T>(k)] = conj(z[pad<T>(W - k)]);
-          if (g.rank == 0) z[0].y = T(0);
+          for (int k = A.Wc + g.rank; k < W; k += g.size()) z[lay(k)] = conj(z[lay(W - k)]);
+          if (g.rank == 0) z[lay(0)].y = T(0);
           g.sync();
         }
-        fft_line<T, +1, FS>(z, A.fft, g);
-        if (i >= off && i < off + nb)
-          for (int x = g.rank; x < W; x += g.size) bad |= !finite_(L.get(i, x));
+        fft_line<T, +1, FS>(z, A.fft, g, lay);
+        if (own)
+          for (int x = g.rank; x < W; x += g.size()) bad |= !finite_(L.get(i, x));
       }
     }
     if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, MODE == MODE_F0 ? 0 : A.iter);
@@ -288,6 +330,14 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     if (MODE == MODE_FIN) {
       double e = 0.0;
       T* upl = A.u + (size_t)b * A.u_ps;
+      if (PACKED && !trace) {
+        const int np = W / 2;
+        for (int t = tid; t < nb * np; t += nthr) {
+          const int j = t / np, q = t - j * np;
+          reinterpret_cast<cx<T>*>(upl + (size_t)(r0 + j) * A.u_rp)[q] = L.line(j + off)[lay(q)];
+        }
+        return;
+      }
       for (int t = tid; t < nb * W; t += nthr) {
         const int j = t / W, x = t - j * W;
         const T uc = L.get(j + off, x);
@@ -309,10 +359,12 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     // ---------------- phase B: fused stencil -> rhs rows (lines 0..nb-1)
     // Each thread walks down a QW-column strip carrying mu_y of the row above
     // in registers.  Line j+1 holds row r0+j; rhs of row r0+j is written into
-    // line j once every thread is past row r0+j-1.
-    constexpr int QW = WIDE ? 8 : 4, GMAX = 4;  // columns per strip, strips per thread
+    // line j once every thread is past row r0+j-1.  f of the next row is
+    // prefetched into registers one row ahead.
+    constexpr int QW = WIDE ? 8 : 4, GMAX = 4;
     const int ng = (W + QW - 1) / QW;
     T myup[GMAX][QW];
+    T fcur[GMAX][QW];
     double e = 0.0;
 #pragma unroll
     for (int gi = 0; gi < GMAX; ++gi) {
@@ -321,19 +373,25 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
 #pragma unroll
         for (int q = 0; q < QW; ++q) {
           const int x = gg * QW + q;
-          if (x < W) myup[gi][q] = aux(L.get(1, x) - L.get(0, x), P);
+          myup[gi][q] = x < W ? aux(L.get(1, x) - L.get(0, x), P) : T(0);
+          fcur[gi][q] = (MODE == MODE_IT && x < W) ? __ldg(fpl + (size_t)r0 * A.f_rp + x) : T(0);
         }
       }
     }
     for (int j = 0; j < nb; ++j) {
       const int i = j + 1;
-      const T* frow = (MODE == MODE_IT) ? fpl + (size_t)(r0 + j) * A.f_rp : nullptr;
       T rhs[GMAX][QW];
+      T fnext[GMAX][QW];
 #pragma unroll
       for (int gi = 0; gi < GMAX; ++gi) {
         const int gg = tid + gi * nthr;
         if (gg < ng) {
           const int x0 = gg * QW;
+          if (MODE == MODE_IT) {
+            const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp;
+#pragma unroll
+            for (int q = 0; q < QW; ++q) fnext[gi][q] = x0 + q < W ? __ldg(fr + x0 + q) : T(0);
+          }
           T uc[QW], ud[QW];
 #pragma unroll
           for (int q = 0; q < QW; ++q) {
@@ -352,7 +410,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
               const T mxq = aux(gx, P);
               const T myq = aux(gy, P);
               const T a = (mxp - mxq) + (myup[gi][q] - myq);
-              const T fv = (MODE == MODE_F0) ? uc[q] : frow[x];
+              const T fv = (MODE == MODE_F0) ? uc[q] : fcur[gi][q];
               rhs[gi][q] = fv + P.lam2 * a;
               if (trace) {
                 const T d = uc[q] - fv;
@@ -373,6 +431,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
           for (int q = 0; q < QW; ++q) {
             const int x = gg * QW + q;
             if (x < W) L.set(j, x, rhs[gi][q]);
+            fcur[gi][q] = fnext[gi][q];
           }
         }
       }
@@ -387,24 +446,27 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   // ---------------- phase C: r2c of rhs rows -> S_out (group per line)
   for (int i = g.id; i < nb; i += ngroups) {
     cx<T>* z = L.line(i);
-    fft_line<T, -1, FS>(z, A.fft, g);
-    if (PACKED) r2c_post<T>(z, A.N, A.wreal, g);
+    fft_line<T, -1, FS>(z, A.fft, g, lay);
+    if (PACKED) r2c_post<T>(z, A.N, A.wreal, g, lay);
     cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
-    for (int k = g.rank; k < A.Wc; k += g.size) dst[k] = z[pad<T>(k)];
+    for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[lay(k)];
   }
 }
 
 // ------------------------------------------------------------ column pass
-// A strip of C columns is loaded transposed into C padded lines (line pitch
-// LPc chosen so the transposing load/store is bank-conflict-free); a group
-// owns one column at a time: forward FFT, * 1/(H W denom), inverse FFT.
+// A strip of C columns is loaded transposed into C lines (line pitch CS
+// chosen so the transposing copies are bank-conflict-free); a group owns one
+// column at a time: forward FFT, * 1/(H W denom), inverse FFT.
 template <typename T, class FS>
 __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
+  using Grp = GroupT<FS::G>;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const Group g{tid / A.fft.G, A.fft.G, tid % A.fft.G};
-  const int ngroups = nthr / A.fft.G;
+  const int G = FS::G > 0 ? FS::G : A.fft.G;
+  const Grp g{tid / G, G, tid % G};
+  const int ngroups = nthr / G;
+  const auto lay = FS::template layout<T>(A.fft);
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * A.C;
   const int nc = min(A.C, A.Wc - c0);
@@ -412,30 +474,31 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
   cx<T>* Spl = A.S + (size_t)b * A.S_ps + c0;
   for (int t = tid; t < H * nc; t += nthr) {
     const int y = t / nc, c = t - y * nc;
-    tile[c * A.CS + pad<T>(y)] = Spl[(size_t)y * A.S_rp + c];
+    cp_async<sizeof(cx<T>)>(tile + c * A.CS + lay(y), Spl + (size_t)y * A.S_rp + c);
   }
+  cp_async_wait_all();
   __syncthreads();
   for (int c = g.id; c < nc; c += ngroups) {
     cx<T>* z = tile + c * A.CS;
-    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g);
+    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g, lay);
     if (A.mode == COL_SOLVE) {
       // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses
       const T wxc = __ldg(A.wx + c0 + c);
-      for (int y = g.rank; y < H; y += g.size) {
+      for (int y = g.rank; y < H; y += g.size()) {
         const T d = T(1) + A.cl2 * (__ldg(A.wy + y) + wxc);
-        z[pad<T>(y)] = scale(z[pad<T>(y)], A.inv_hw / d);
+        z[lay(y)] = scale(z[lay(y)], A.inv_hw / d);
       }
       g.sync();
     } else if (A.mode == COL_INV) {
-      for (int y = g.rank; y < H; y += g.size) z[pad<T>(y)] = scale(z[pad<T>(y)], A.inv_hw);
+      for (int y = g.rank; y < H; y += g.size()) z[lay(y)] = scale(z[lay(y)], A.inv_hw);
       g.sync();
     }
-    if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g);
+    if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g, lay);
   }
   __syncthreads();
   for (int t = tid; t < H * nc; t += nthr) {
     const int y = t / nc, c = t - y * nc;
-    Spl[(size_t)y * A.S_rp + c] = tile[c * A.CS + pad<T>(y)];
+    Spl[(size_t)y * A.S_rp + c] = tile[c * A.CS + lay(y)];
   }
 }
 
@@ -477,10 +540,11 @@ __global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long n
 // Compile-time FFT plans for the hot sizes (fp32).  Everything else runs the
 // runtime-planned path (FftRt).  The host planner (ils_api.cu) uses exactly
 // these radix lists when n matches, so twiddle tables and kernels agree.
-#define ILS_ROW_SPECS(X) X(0, 256, 16, 16) X(1, 960, 16, 15, 4) X(2, 1920, 16, 15, 8) X(3, 3840, 16, 16, 15) X(4, 512, 16, 8, 4)
+// X(id, swizzle, group threads, n, radices...)
+#define ILS_ROW_SPECS(X) X(0, 1, 32, 256, 16, 16) X(1, 1, 64, 960, 16, 15, 4) X(2, 1, 128, 1920, 16, 15, 8) X(3, 1, 256, 3840, 16, 16, 15) X(4, 1, 32, 512, 16, 8, 4)
 // row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
 #define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)
-#define ILS_COL_SPECS(X) X(0, 512, 16, 8, 4) X(1, 1080, 15, 9, 8) X(2, 2160, 16, 15, 9) X(3, 4320, 16, 15, 9, 2) X(4, 256, 16, 16)
+#define ILS_COL_SPECS(X) X(0, 1, 32, 512, 16, 8, 4) X(1, 0, 128, 1080, 15, 9, 8) X(2, 1, 256, 2160, 16, 15, 9) X(3, 1, 32, 256, 16, 16) X(4, 1, 128, 720, 16, 9, 5)
 
 template <int ID>
 struct RowSpec;
