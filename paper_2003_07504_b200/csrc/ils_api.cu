@@ -201,12 +201,20 @@ bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
   long long Ns = 1;
   for (int R : out.radix) {
     out.tw_off.push_back((int)(out.tw.size() / 2));
-    for (long long m = 0; m < Ns; ++m)
-      for (int r = 1; r < R; ++r) {
-        const sc_t w = sincos2pi(-(long long)r * m, Ns * R);
+    if (R <= 16) {  // unrolled radices: w^m only, powers formed in registers
+      for (long long m = 0; m < Ns; ++m) {
+        const sc_t w = sincos2pi(-m, Ns * R);
         out.tw.push_back(w.c);
         out.tw.push_back(w.s);
       }
+    } else {
+      for (long long m = 0; m < Ns; ++m)
+        for (int r = 1; r < R; ++r) {
+          const sc_t w = sincos2pi(-(long long)r * m, Ns * R);
+          out.tw.push_back(w.c);
+          out.tw.push_back(w.s);
+        }
+    }
     out.gen_off.push_back((int)(out.tw.size() / 2));
     if (R > 16)
       for (int q = 0; q < R; ++q) {
@@ -327,7 +335,7 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
         bestCS = CS;
       }
     }
-    const size_t smem = (size_t)C * bestCS * elt;
+    const size_t smem = (size_t)C * bestCS * elt + (size_t)p.H * (elt / 2);  // tile + wy
     if (smem > 227 * 1024) break;
     const int per_sm = smem <= 113 * 1024 ? 2 : 1;
     const long strips = (p.Wc + C - 1) / C;
@@ -380,7 +388,8 @@ PenaltyDev<T> pen_dev(const ils_params& q) {
   P.ph = T(q.p / 2.0);
   P.eps = T(q.eps);
   const double g2 = q.gamma * q.gamma;
-  P.wk = q.kind == ILS_WELSCH ? T(-1.0 / (2.0 * g2)) : T(0);
+  const double log2e = sizeof(T) == 4 ? 1.4426950408889634 : 1.0;  // fp32 exp via ex2
+  P.wk = q.kind == ILS_WELSCH ? T(-log2e / (2.0 * g2)) : T(0);
   P.g2x2 = T(2.0 * g2);
   P.c = T(q.c);
   P.lam = T(q.lam);

@@ -21,9 +21,10 @@
 // conflict without it; radix-15 first passes conflict with it); the host
 // planner simulates the bank traffic of both and picks per plan.
 //
-// Twiddles come from a per-pass table [m][r-1] computed on the host in double
-// with exact integer angle reduction.  Radices 2..16 are unrolled; odd primes
-// 17..61 use a looped direct DFT (generic sizes only).
+// Twiddles: one table entry w_{Ns R}^m per butterfly class, computed on the
+// host in double with exact integer angle reduction; powers in registers.
+// Radices 2..16 are unrolled; odd primes 17..61 use a looped direct DFT
+// (generic sizes only).
 #pragma once
 
 #include "ils_dft.cuh"
@@ -40,7 +41,7 @@ struct FftDev {
   int G;        // threads per line group
   int laymask;  // swizzle mask of the line layout (0 = identity)
   int radix[kMaxPass];
-  int tw_off[kMaxPass];   // pass twiddles: Ns*(R-1) entries, layout [m][r-1]
+  int tw_off[kMaxPass];   // pass twiddles: R<=16: Ns entries w^m; generic R: Ns*(R-1), [m][r-1]
   int gen_off[kMaxPass];  // generic primes: R entries w_R^q
   const cx<T>* tw;
 };
@@ -133,12 +134,15 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
 #pragma unroll
     for (int r = 0; r < R; ++r) v[k][r] = x[lay(j + r * nb)];
     if (Ns > 1) {
-      const cx<T>* w = tw + (j % Ns) * (R - 1);
+      // one table load per butterfly: w = w_{Ns R}^(j mod Ns); the powers
+      // w^r by running product (<= 15 roundings, ~1e-6 relative in fp32)
+      cx<T> w1 = ldtw(tw + (j % Ns));
+      if (DIR > 0) w1.y = -w1.y;
+      cx<T> w = w1;
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        cx<T> ww = ldtw(w + r - 1);
-        if (DIR > 0) ww.y = -ww.y;
-        v[k][r] = cmul(v[k][r], ww);
+        v[k][r] = cmul(v[k][r], w);
+        if (r + 1 < R) w = cmul(w, w1);
       }
     }
     dft<R, DIR>(v[k]);

@@ -40,7 +40,7 @@ struct PenaltyDev {
   T pe;       // p/2 - 1
   T ph;       // p/2
   T eps;
-  T wk;       // Welsch: -1/(2 g^2)  (natural-log scale)
+  T wk;       // Welsch: -1/(2 g^2), times log2(e) for fp32 (ex2-based exp)
   T g2x2;     // Welsch: 2 g^2
   T c;        // curvature
   T lam;
@@ -86,31 +86,57 @@ struct ColArgs {
 };
 
 // ------------------------------------------------------------ penalty math
-__device__ __forceinline__ float fpow_pos(float q, float e) { return exp2f(e * __log2f(q)); }
+// fp32 uses the SFU directly (lg2/ex2.approx.ftz: ~2 ulp); fp64 uses libm.
+__device__ __forceinline__ float lg2_fast(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fpow_pos(float q, float e) { return ex2_fast(__fmul_rn(e, lg2_fast(q))); }
 __device__ __forceinline__ double fpow_pos(double q, double e) { return pow(q, e); }
-__device__ __forceinline__ float fexp(float x) { return __expf(x); }
-__device__ __forceinline__ double fexp(double x) { return exp(x); }
+// exp(x * k) with k pre-scaled by log2(e) for fp32
+__device__ __forceinline__ float fexp_scaled(float x) { return ex2_fast(x); }
+__device__ __forceinline__ double fexp_scaled(double x) { return exp(x); }
 
 // phi'(x): penalty.py:64-66 (Charbonnier), 93-96 (Welsch)
 template <typename T>
 __device__ __forceinline__ T dphi(T x, const PenaltyDev<T>& P) {
   if (P.kind == 0) return P.p * x * fpow_pos(x * x + P.eps, P.pe);
-  return T(2) * x * fexp(x * x * P.wk);
+  return T(2) * x * fexp_scaled(x * x * P.wk);
 }
 // phi(x): penalty.py:60-62, 88-91 (trace only)
 template <typename T>
 __device__ __forceinline__ T phi(T x, const PenaltyDev<T>& P) {
   if (P.kind == 0) return fpow_pos(x * x + P.eps, P.ph);
-  return P.g2x2 * (T(1) - fexp(x * x * P.wk));
+  return P.g2x2 * (T(1) - fexp_scaled(x * x * P.wk));
 }
-// mu = c x - phi'(x): penalty.py:117-126
+// Explicitly rounded primitives: the compiler never contracts these, so the
+// same pixel computes bit-identical mu wherever it sits in a band (placement
+// invariance, the multi-GPU / batch-size bitwise-equality contract).
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// mu = c x - phi'(x) = x (c - p (x^2+eps)^(p/2-1)) (Charbonnier) or
+// x (c - 2 exp(-x^2/2g^2)) (Welsch): penalty.py:117-126
 template <typename T>
 __device__ __forceinline__ T aux(T x, const PenaltyDev<T>& P) {
-  return P.c * x - dphi(x, P);
+  const T q = fma_rn(x, x, P.kind == 0 ? P.eps : T(0));
+  const T t = P.kind == 0 ? fpow_pos(q, P.pe) : fexp_scaled(mul_rn(q, P.wk));
+  return mul_rn(x, fma_rn(P.kind == 0 ? -P.p : T(-2), t, P.c));
 }
 
 template <typename T>
 __device__ __forceinline__ bool finite_(T v) { return isfinite(v); }
+
+__device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fast_div(double a, double b) { return a / b; }
 
 // ------------------------------------------------------------ line access
 // Line i of a row CTA starts at lines + i*LP (complex slots, layout Lay).
@@ -129,6 +155,27 @@ struct Lines {
   __device__ __forceinline__ void set(int i, int x, T v) const {
     if (PACKED) reinterpret_cast<T*>(line(i))[2 * lay(x >> 1) + (x & 1)] = v;
     else line(i)[lay(x)] = cx<T>{v, T(0)};
+  }
+  // QW consecutive reals from x0 (QW | x0, packed lines): complex elements
+  // x0/2 .. x0/2 + QW/2 - 1 share one 128-byte block, so their slots are
+  // lay(x0/2) ^ q -- one index computation per strip.
+  template <int QW>
+  __device__ __forceinline__ void get_strip(int i, int x0, T (&v)[QW]) const {
+    const cx<T>* z = line(i);
+    const int s = lay(x0 >> 1);
+#pragma unroll
+    for (int q = 0; q < QW / 2; ++q) {
+      const cx<T> c = z[s ^ q];
+      v[2 * q] = c.x;
+      v[2 * q + 1] = c.y;
+    }
+  }
+  template <int QW>
+  __device__ __forceinline__ void set_strip(int i, int x0, const T (&v)[QW]) const {
+    cx<T>* z = line(i);
+    const int s = lay(x0 >> 1);
+#pragma unroll
+    for (int q = 0; q < QW / 2; ++q) z[s ^ q] = cx<T>{v[2 * q], v[2 * q + 1]};
   }
 };
 
@@ -308,8 +355,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
       if (MODE == MODE_F0) {
         if (!PACKED)
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
-        if (own)
-          for (int x = g.rank; x < W; x += g.size()) bad |= !finite_(L.get(i, x));
       } else {
         if (PACKED) {
           c2r_pre<T>(z, A.N, A.wreal, g, lay);
@@ -320,11 +365,10 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
           g.sync();
         }
         fft_line<T, +1, FS>(z, A.fft, g, lay);
-        if (own)
-          for (int x = g.rank; x < W; x += g.size()) bad |= !finite_(L.get(i, x));
       }
+      (void)own;
     }
-    if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, MODE == MODE_F0 ? 0 : A.iter);
+    __syncthreads();
 
     // ---------------- final pass: write u (and its energy)
     if (MODE == MODE_FIN) {
@@ -332,15 +376,22 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
       T* upl = A.u + (size_t)b * A.u_ps;
       if (PACKED && !trace) {
         const int np = W / 2;
-        for (int t = tid; t < nb * np; t += nthr) {
-          const int j = t / np, q = t - j * np;
-          reinterpret_cast<cx<T>*>(upl + (size_t)(r0 + j) * A.u_rp)[q] = L.line(j + off)[lay(q)];
+        for (int j = 0; j < nb; ++j) {
+          cx<T>* dst = reinterpret_cast<cx<T>*>(upl + (size_t)(r0 + j) * A.u_rp);
+          const cx<T>* z = L.line(j + off);
+          for (int q = tid; q < np; q += nthr) {
+            const cx<T> v = z[lay(q)];
+            bad |= !(finite_(v.x) && finite_(v.y));
+            dst[q] = v;
+          }
         }
+        if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, A.iter);
         return;
       }
       for (int t = tid; t < nb * W; t += nthr) {
         const int j = t / W, x = t - j * W;
         const T uc = L.get(j + off, x);
+        bad |= !finite_(uc);
         upl[(size_t)(r0 + j) * A.u_rp + x] = uc;
         if (trace) {
           const T gx = L.get(j + off, wrapi(x + 1, W)) - uc;
@@ -349,6 +400,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
           e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
         }
       }
+      if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, A.iter);
       if (trace) {
         const double s = block_sum(e, red);
         if (tid == 0) A.epart[(size_t)b * gridDim.x + blockIdx.x] = s;
@@ -380,7 +432,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     }
     for (int j = 0; j < nb; ++j) {
       const int i = j + 1;
-      T rhs[GMAX][QW];
+      T rhs[GMAX][QW] = {};
       T fnext[GMAX][QW];
 #pragma unroll
       for (int gi = 0; gi < GMAX; ++gi) {
@@ -393,12 +445,19 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
             for (int q = 0; q < QW; ++q) fnext[gi][q] = x0 + q < W ? __ldg(fr + x0 + q) : T(0);
           }
           T uc[QW], ud[QW];
+          if (PACKED && x0 + QW <= W) {
+            L.template get_strip<QW>(i, x0, uc);
+            L.template get_strip<QW>(i + 1, x0, ud);
+          } else {
 #pragma unroll
-          for (int q = 0; q < QW; ++q) {
-            const int x = x0 + q;
-            uc[q] = x < W ? L.get(i, x) : T(0);
-            ud[q] = x < W ? L.get(i + 1, x) : T(0);
+            for (int q = 0; q < QW; ++q) {
+              const int x = x0 + q;
+              uc[q] = x < W ? L.get(i, x) : T(0);
+              ud[q] = x < W ? L.get(i + 1, x) : T(0);
+            }
           }
+#pragma unroll
+          for (int q = 0; q < QW; ++q) bad |= !finite_(uc[q]);
           T mxp = aux(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
 #pragma unroll
           for (int q = 0; q < QW; ++q) {
@@ -411,7 +470,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
               const T myq = aux(gy, P);
               const T a = (mxp - mxq) + (myup[gi][q] - myq);
               const T fv = (MODE == MODE_F0) ? uc[q] : fcur[gi][q];
-              rhs[gi][q] = fv + P.lam2 * a;
+              rhs[gi][q] = fma_rn(P.lam2, a, fv);
               if (trace) {
                 const T d = uc[q] - fv;
                 e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
@@ -427,16 +486,22 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
       for (int gi = 0; gi < GMAX; ++gi) {
         const int gg = tid + gi * nthr;
         if (gg < ng) {
+          const int x0 = gg * QW;
+          if (PACKED && x0 + QW <= W) {
+            L.template set_strip<QW>(j, x0, rhs[gi]);
+          } else {
 #pragma unroll
-          for (int q = 0; q < QW; ++q) {
-            const int x = gg * QW + q;
-            if (x < W) L.set(j, x, rhs[gi][q]);
-            fcur[gi][q] = fnext[gi][q];
+            for (int q = 0; q < QW; ++q)
+              if (x0 + q < W) L.set(j, x0 + q, rhs[gi][q]);
           }
+#pragma unroll
+          for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
         }
       }
     }
-    __syncthreads();
+    // the stencil read every band row of u once: flag the first non-finite
+    // iterate (0 = non-finite input plane), smoother.py:166-167 / image.py:43-44
+    if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, MODE == MODE_F0 ? 0 : A.iter);
     if (trace) {
       const double s = block_sum(e, red);
       if (tid == 0) A.epart[(size_t)b * gridDim.x + blockIdx.x] = s;
@@ -461,6 +526,7 @@ template <typename T, class FS>
 __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
+  T* swy = reinterpret_cast<T*>(tile + A.C * A.CS);  // wy[0..H) staged once per CTA
   using Grp = GroupT<FS::G>;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = FS::G > 0 ? FS::G : A.fft.G;
@@ -472,10 +538,13 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
   const int nc = min(A.C, A.Wc - c0);
   const int H = A.H;
   cx<T>* Spl = A.S + (size_t)b * A.S_ps + c0;
-  for (int t = tid; t < H * nc; t += nthr) {
-    const int y = t / nc, c = t - y * nc;
-    cp_async<sizeof(cx<T>)>(tile + c * A.CS + lay(y), Spl + (size_t)y * A.S_rp + c);
-  }
+  // transposing copies: thread -> (column cc, first row y0), rows step ystep
+  const int ystep = nthr / nc, cc = tid % nc, y0 = tid / nc;
+  const bool copier = tid < ystep * nc;
+  if (copier)
+    for (int y = y0; y < H; y += ystep) cp_async<sizeof(cx<T>)>(tile + cc * A.CS + lay(y), Spl + (size_t)y * A.S_rp + cc);
+  if (A.mode == COL_SOLVE)
+    for (int y = tid; y < H; y += nthr) swy[y] = __ldg(A.wy + y);
   cp_async_wait_all();
   __syncthreads();
   for (int c = g.id; c < nc; c += ngroups) {
@@ -483,10 +552,11 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
     if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g, lay);
     if (A.mode == COL_SOLVE) {
       // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses
-      const T wxc = __ldg(A.wx + c0 + c);
+      const T base = T(1) + A.cl2 * __ldg(A.wx + c0 + c);
+#pragma unroll 4
       for (int y = g.rank; y < H; y += g.size()) {
-        const T d = T(1) + A.cl2 * (__ldg(A.wy + y) + wxc);
-        z[lay(y)] = scale(z[lay(y)], A.inv_hw / d);
+        const T d = base + A.cl2 * swy[y];
+        z[lay(y)] = scale(z[lay(y)], fast_div(A.inv_hw, d));
       }
       g.sync();
     } else if (A.mode == COL_INV) {
@@ -496,10 +566,8 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
     if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g, lay);
   }
   __syncthreads();
-  for (int t = tid; t < H * nc; t += nthr) {
-    const int y = t / nc, c = t - y * nc;
-    Spl[(size_t)y * A.S_rp + c] = tile[c * A.CS + lay(y)];
-  }
+  if (copier)
+    for (int y = y0; y < H; y += ystep) Spl[(size_t)y * A.S_rp + cc] = tile[cc * A.CS + lay(y)];
 }
 
 // ------------------------------------------------------------ small kernels
