@@ -388,8 +388,11 @@ PenaltyDev<T> pen_dev(const ils_params& q) {
   P.ph = T(q.p / 2.0);
   P.eps = T(q.eps);
   const double g2 = q.gamma * q.gamma;
-  const double log2e = sizeof(T) == 4 ? 1.4426950408889634 : 1.0;  // fp32 exp via ex2
+  const double log2e = 1.4426950408889634;  // exp(x) = 2^(x log2 e)
   P.wk = q.kind == ILS_WELSCH ? T(-log2e / (2.0 * g2)) : T(0);
+  P.eps0 = q.kind == ILS_CHARBONNIER ? T(q.eps) : T(0);
+  P.E = q.kind == ILS_CHARBONNIER ? T(q.p / 2.0 - 1.0) : P.wk;
+  P.coef = q.kind == ILS_CHARBONNIER ? T(-q.p) : T(-2.0);
   P.g2x2 = T(2.0 * g2);
   P.c = T(q.c);
   P.lam = T(q.lam);

@@ -40,11 +40,14 @@ struct PenaltyDev {
   T pe;       // p/2 - 1
   T ph;       // p/2
   T eps;
-  T wk;       // Welsch: -1/(2 g^2), times log2(e) for fp32 (ex2-based exp)
+  T wk;       // Welsch: -log2(e) / (2 g^2)   (exp via exp2)
   T g2x2;     // Welsch: 2 g^2
   T c;        // curvature
   T lam;
   T lam2;     // lam / 2
+  // branch-free mu = x * (c + coef * 2^(E * Lg)), Lg = log2(x^2 + eps0)
+  // (Charbonnier) or x^2 (Welsch): one code path for both families
+  T eps0, E, coef;
 };
 
 template <typename T>
@@ -87,34 +90,19 @@ struct ColArgs {
 
 // ------------------------------------------------------------ penalty math
 // fp32 uses the SFU directly (lg2/ex2.approx.ftz: ~2 ulp); fp64 uses libm.
-__device__ __forceinline__ float lg2_fast(float x) {
+__device__ __forceinline__ float lg2_(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float ex2_fast(float x) {
+__device__ __forceinline__ float ex2_(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float fpow_pos(float q, float e) { return ex2_fast(__fmul_rn(e, lg2_fast(q))); }
-__device__ __forceinline__ double fpow_pos(double q, double e) { return pow(q, e); }
-// exp(x * k) with k pre-scaled by log2(e) for fp32
-__device__ __forceinline__ float fexp_scaled(float x) { return ex2_fast(x); }
-__device__ __forceinline__ double fexp_scaled(double x) { return exp(x); }
+__device__ __forceinline__ double lg2_(double x) { return log2(x); }
+__device__ __forceinline__ double ex2_(double x) { return exp2(x); }
 
-// phi'(x): penalty.py:64-66 (Charbonnier), 93-96 (Welsch)
-template <typename T>
-__device__ __forceinline__ T dphi(T x, const PenaltyDev<T>& P) {
-  if (P.kind == 0) return P.p * x * fpow_pos(x * x + P.eps, P.pe);
-  return T(2) * x * fexp_scaled(x * x * P.wk);
-}
-// phi(x): penalty.py:60-62, 88-91 (trace only)
-template <typename T>
-__device__ __forceinline__ T phi(T x, const PenaltyDev<T>& P) {
-  if (P.kind == 0) return fpow_pos(x * x + P.eps, P.ph);
-  return P.g2x2 * (T(1) - fexp_scaled(x * x * P.wk));
-}
 // Explicitly rounded primitives: the compiler never contracts these, so the
 // same pixel computes bit-identical mu wherever it sits in a band (placement
 // invariance, the multi-GPU / batch-size bitwise-equality contract).
@@ -123,13 +111,21 @@ __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 
-// mu = c x - phi'(x) = x (c - p (x^2+eps)^(p/2-1)) (Charbonnier) or
-// x (c - 2 exp(-x^2/2g^2)) (Welsch): penalty.py:117-126
+// mu = c x - phi'(x) (penalty.py:117-126) with phi' from penalty.py:64-66
+// (Charbonnier: p x (x^2+eps)^(p/2-1)) or 93-96 (Welsch: 2x exp(-x^2/2g^2)),
+// written as x * (c + coef * 2^(E * Lg)).
 template <typename T>
 __device__ __forceinline__ T aux(T x, const PenaltyDev<T>& P) {
-  const T q = fma_rn(x, x, P.kind == 0 ? P.eps : T(0));
-  const T t = P.kind == 0 ? fpow_pos(q, P.pe) : fexp_scaled(mul_rn(q, P.wk));
-  return mul_rn(x, fma_rn(P.kind == 0 ? -P.p : T(-2), t, P.c));
+  const T q = fma_rn(x, x, P.eps0);
+  const T lg = P.kind == 0 ? lg2_(q) : q;
+  const T t = ex2_(mul_rn(P.E, lg));
+  return mul_rn(x, fma_rn(P.coef, t, P.c));
+}
+// phi(x): penalty.py:60-62, 88-91 (energy trace only)
+template <typename T>
+__device__ __forceinline__ T phi(T x, const PenaltyDev<T>& P) {
+  if (P.kind == 0) return ex2_(P.ph * lg2_(x * x + P.eps));
+  return P.g2x2 * (T(1) - ex2_(x * x * P.wk));
 }
 
 template <typename T>
@@ -415,92 +411,102 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     // prefetched into registers one row ahead.
     constexpr int QW = WIDE ? 8 : 4, GMAX = 4;
     const int ng = (W + QW - 1) / QW;
-    T myup[GMAX][QW];
-    T fcur[GMAX][QW];
+    const bool is_it = MODE == MODE_IT;
+    T chk = T(0);  // fma(x, 0, chk) turns NaN on any non-finite x
     double e = 0.0;
-#pragma unroll
-    for (int gi = 0; gi < GMAX; ++gi) {
-      const int gg = tid + gi * nthr;
-      if (gg < ng) {
-#pragma unroll
-        for (int q = 0; q < QW; ++q) {
-          const int x = gg * QW + q;
-          myup[gi][q] = x < W ? aux(L.get(1, x) - L.get(0, x), P) : T(0);
-          fcur[gi][q] = (MODE == MODE_IT && x < W) ? __ldg(fpl + (size_t)r0 * A.f_rp + x) : T(0);
-        }
-      }
-    }
-    for (int j = 0; j < nb; ++j) {
-      const int i = j + 1;
-      T rhs[GMAX][QW] = {};
-      T fnext[GMAX][QW];
+    auto band = [&](auto trace_tag) {
+      constexpr bool TR = decltype(trace_tag)::value;
+      T myup[GMAX][QW];
+      T fcur[GMAX][QW];
 #pragma unroll
       for (int gi = 0; gi < GMAX; ++gi) {
         const int gg = tid + gi * nthr;
         if (gg < ng) {
-          const int x0 = gg * QW;
-          if (MODE == MODE_IT) {
-            const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp;
-#pragma unroll
-            for (int q = 0; q < QW; ++q) fnext[gi][q] = x0 + q < W ? __ldg(fr + x0 + q) : T(0);
-          }
-          T uc[QW], ud[QW];
-          if (PACKED && x0 + QW <= W) {
-            L.template get_strip<QW>(i, x0, uc);
-            L.template get_strip<QW>(i + 1, x0, ud);
-          } else {
-#pragma unroll
-            for (int q = 0; q < QW; ++q) {
-              const int x = x0 + q;
-              uc[q] = x < W ? L.get(i, x) : T(0);
-              ud[q] = x < W ? L.get(i + 1, x) : T(0);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < QW; ++q) bad |= !finite_(uc[q]);
-          T mxp = aux(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
 #pragma unroll
           for (int q = 0; q < QW; ++q) {
-            const int x = x0 + q;
-            if (x < W) {
-              const T ur = (q + 1 < QW && x + 1 < W) ? uc[q + 1] : L.get(i, wrapi(x + 1, W));
-              const T gx = ur - uc[q];
-              const T gy = ud[q] - uc[q];
-              const T mxq = aux(gx, P);
-              const T myq = aux(gy, P);
-              const T a = (mxp - mxq) + (myup[gi][q] - myq);
-              const T fv = (MODE == MODE_F0) ? uc[q] : fcur[gi][q];
-              rhs[gi][q] = fma_rn(P.lam2, a, fv);
-              if (trace) {
-                const T d = uc[q] - fv;
-                e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
+            const int x = gg * QW + q;
+            myup[gi][q] = x < W ? aux(L.get(1, x) - L.get(0, x), P) : T(0);
+            fcur[gi][q] = (is_it && x < W) ? __ldg(fpl + (size_t)r0 * A.f_rp + x) : T(0);
+          }
+        }
+      }
+      for (int j = 0; j < nb; ++j) {
+        const int i = j + 1;
+        T rhs[GMAX][QW];
+        T fnext[GMAX][QW];
+#pragma unroll
+        for (int gi = 0; gi < GMAX; ++gi) {
+          const int gg = tid + gi * nthr;
+          if (gg < ng) {
+            const int x0 = gg * QW;
+            const bool full = PACKED && x0 + QW <= W;
+            if (is_it) {
+              const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp + x0;
+#pragma unroll
+              for (int q = 0; q < QW; ++q) fnext[gi][q] = (full || x0 + q < W) ? __ldg(fr + q) : T(0);
+            }
+            T uc[QW], ud[QW];
+            if (full) {
+              L.template get_strip<QW>(i, x0, uc);
+              L.template get_strip<QW>(i + 1, x0, ud);
+            } else {
+#pragma unroll
+              for (int q = 0; q < QW; ++q) {
+                const int x = x0 + q;
+                uc[q] = x < W ? L.get(i, x) : T(0);
+                ud[q] = x < W ? L.get(i + 1, x) : T(0);
               }
-              myup[gi][q] = myq;
-              mxp = mxq;
+            }
+            T mxp = aux(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
+            const T uright = L.get(i, wrapi(full ? x0 + QW : min(x0 + QW, W), W));
+#pragma unroll
+            for (int q = 0; q < QW; ++q) {
+              if (full || x0 + q < W) {
+                const T ur = (q + 1 < QW && (full || x0 + q + 1 < W)) ? uc[q + 1] : uright;
+                const T gx = ur - uc[q];
+                const T gy = ud[q] - uc[q];
+                const T mxq = aux(gx, P);
+                const T myq = aux(gy, P);
+                const T a = (mxp - mxq) + (myup[gi][q] - myq);
+                const T fv = is_it ? fcur[gi][q] : uc[q];
+                rhs[gi][q] = fma_rn(P.lam2, a, fv);
+                chk = fma_rn(uc[q], T(0), chk);
+                if constexpr (TR) {
+                  const T d = uc[q] - fv;
+                  e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
+                }
+                myup[gi][q] = myq;
+                mxp = mxq;
+              } else {
+                rhs[gi][q] = T(0);
+              }
             }
           }
         }
-      }
-      __syncthreads();
+        __syncthreads();
 #pragma unroll
-      for (int gi = 0; gi < GMAX; ++gi) {
-        const int gg = tid + gi * nthr;
-        if (gg < ng) {
-          const int x0 = gg * QW;
-          if (PACKED && x0 + QW <= W) {
-            L.template set_strip<QW>(j, x0, rhs[gi]);
-          } else {
+        for (int gi = 0; gi < GMAX; ++gi) {
+          const int gg = tid + gi * nthr;
+          if (gg < ng) {
+            const int x0 = gg * QW;
+            if (PACKED && x0 + QW <= W) {
+              L.template set_strip<QW>(j, x0, rhs[gi]);
+            } else {
 #pragma unroll
-            for (int q = 0; q < QW; ++q)
-              if (x0 + q < W) L.set(j, x0 + q, rhs[gi][q]);
+              for (int q = 0; q < QW; ++q)
+                if (x0 + q < W) L.set(j, x0 + q, rhs[gi][q]);
+            }
+#pragma unroll
+            for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
           }
-#pragma unroll
-          for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
         }
       }
-    }
+    };
+    if (trace) band(std::true_type{});
+    else band(std::false_type{});
     // the stencil read every band row of u once: flag the first non-finite
     // iterate (0 = non-finite input plane), smoother.py:166-167 / image.py:43-44
+    bad = !finite_(chk);
     if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, MODE == MODE_F0 ? 0 : A.iter);
     if (trace) {
       const double s = block_sum(e, red);
@@ -514,7 +520,17 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     fft_line<T, -1, FS>(z, A.fft, g, lay);
     if (PACKED) r2c_post<T>(z, A.N, A.wreal, g, lay);
     cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
-    for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[lay(k)];
+    if (PACKED && sizeof(T) == 4) {
+      // 16-byte stores of element pairs (rows are 32-byte aligned)
+      for (int m = g.rank; 2 * m + 1 < A.Wc; m += g.size()) {
+        const int s = lay(2 * m);
+        const cx<T> a0 = z[s], a1 = z[s ^ 1];
+        reinterpret_cast<float4*>(dst)[m] = make_float4(a0.x, a0.y, a1.x, a1.y);
+      }
+      if ((A.Wc & 1) && g.rank == 0) dst[A.Wc - 1] = z[lay(A.Wc - 1)];
+    } else {
+      for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[lay(k)];
+    }
   }
 }
 
