@@ -259,12 +259,15 @@ constexpr int kColThreads = 256;
 constexpr int kNarrowMaxW = 4 * 4 * kRowThreads;  // stencil: 4 strips x 4 columns per thread
 constexpr int kWideMaxW = 4 * 8 * kRowThreads;
 
-template <typename T, bool PACKED, class FS, bool WIDE>
+// SMODE >= 0: kernel specialised for that mode without trace (the hot
+// kernels; dead phases compiled out keeps the code inside the I-cache);
+// SMODE = -1: any mode from A.mode, optional energy trace.
+template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[32];
   using Grp = GroupT<FS::G>;
-  const int MODE = A.mode;  // block-uniform
+  const int MODE = SMODE >= 0 ? SMODE : A.mode;  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = FS::G > 0 ? FS::G : A.fft.G;
   const Grp g{tid / G, G, tid % G};
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   const int r0 = blockIdx.x * A.band;
   const int nb = min(A.band, A.H - r0);
   const int W = A.W, H = A.H;
-  const bool trace = A.epart != nullptr;
+  const bool trace = SMODE < 0 && A.epart != nullptr;
   const bool halo = (MODE == MODE_F0 || MODE == MODE_IT || (MODE == MODE_FIN && trace));
   const int nl = halo ? nb + 2 : nb;
   const int y0 = halo ? r0 - 1 : r0;
@@ -283,6 +286,11 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   const PenaltyDev<T>& P = A.pen;
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
 
+  if (MODE == MODE_IT && tid < nb && (W * sizeof(T)) % 16 == 0 && (A.f_rp * sizeof(T)) % 16 == 0) {
+    // the stencil reads f one row at a time: pull the band's rows into L2 now
+    const T* row = fpl + (size_t)(r0 + tid) * A.f_rp;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((unsigned)(W * sizeof(T))) : "memory");
+  }
   if (MODE == MODE_MU || MODE == MODE_R2C) {
     // rhs rows straight from global memory; each group owns whole lines.
     bool bf = false, bx = false, by = false;
@@ -409,7 +417,9 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     // in registers.  Line j+1 holds row r0+j; rhs of row r0+j is written into
     // line j once every thread is past row r0+j-1.  f of the next row is
     // prefetched into registers one row ahead.
-    constexpr int QW = WIDE ? 8 : 4, GMAX = 4;
+    constexpr int QW = WIDE ? 8 : 4;
+    // strips per thread: exact for compile-time plans, 4 (W <= 16 * 256) otherwise
+    constexpr int GMAX = FS::n > 0 ? (2 * FS::n / QW + kRowThreads - 1) / kRowThreads : 4;
     const int ng = (W + QW - 1) / QW;
     const bool is_it = MODE == MODE_IT;
     T chk = T(0);  // fma(x, 0, chk) turns NaN on any non-finite x
@@ -655,7 +665,12 @@ cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t 
 #ifdef ILS_DEFINE_LAUNCHERS
 template <typename T, bool PACKED, class FS, bool WIDE>
 cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
-  auto k = k_row<T, PACKED, FS, WIDE>;
+  auto k = k_row<T, PACKED, FS, WIDE, -1>;
+  if (a.epart == nullptr) {
+    if (a.mode == MODE_F0) k = k_row<T, PACKED, FS, WIDE, MODE_F0>;
+    if (a.mode == MODE_IT) k = k_row<T, PACKED, FS, WIDE, MODE_IT>;
+    if (a.mode == MODE_FIN) k = k_row<T, PACKED, FS, WIDE, MODE_FIN>;
+  }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, threads, smem, s>>>(a);
