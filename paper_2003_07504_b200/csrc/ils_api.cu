@@ -147,7 +147,12 @@ double bank_cost(int n, const std::vector<int>& radix, int G, bool swz, int E, i
   };
   double tot = 0, ideal = 0;
   int Ns = 1;
-  for (int R : radix) {
+  const int np = (int)radix.size();
+  for (int pi = 0; pi < np; ++pi) {
+    const int R = radix[pi];
+    // lines are identity-laid at both ends of the transform (ils_fft.cuh)
+    auto lay_in = [&](int e) { return pi == 0 ? e : lay(e); };
+    auto lay_out = [&](int e) { return pi == np - 1 ? e : lay(e); };
     const int nb = n / R, km = R <= 16 ? std::max(1, maxe / R) : 1;
     for (int k = 0; k < km; ++k)
       for (int w0 = 0; w0 < G; w0 += 32) {
@@ -157,8 +162,8 @@ double bank_cost(int n, const std::vector<int>& radix, int G, bool swz, int E, i
           for (int l = 0; l < 32; ++l) {
             const int j = w0 + l + k * G;
             act[l] = j < nb;
-            ld[l] = lay(j + r * nb);
-            st[l] = lay((j - j % Ns) * R + j % Ns + r * Ns);
+            ld[l] = lay_in(j + r * nb);
+            st[l] = lay_out((j - j % Ns) * R + j % Ns + r * Ns);
           }
           wave(ld, act, 32, tot, ideal);
           wave(st, act, 32, tot, ideal);
@@ -279,7 +284,7 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   // b+2 lines c2r and b lines r2c; 2 CTAs fit an SM while smem <= ~113 KB.
   const int force = env_int("ILS_ROW_BAND", 0);
   double best = 1e300;
-  for (int band = 1; band <= std::min(p.H, 24); ++band) {
+  for (int band = 1; band <= std::min(p.H, kMaxBandLines - 2); ++band) {
     if (force && band != std::min(force, p.H)) continue;
     const size_t smem = (size_t)(band + 2) * LP * elt;
     if (smem > 227 * 1024) break;
@@ -325,7 +330,7 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
         int cnt[16] = {0};
         for (int t = t0; t < t0 + E; ++t) {
           const int y = t / C, c = t % C;
-          const int e = c * CS + (p.colf.swz ? (y ^ ((y >> (E == 16 ? 4 : 3)) & (E - 1))) : y);
+          const int e = c * CS + y;  // tile lines are identity-laid outside the FFT passes
           cnt[e % E]++;
         }
         tot += *std::max_element(cnt, cnt + E);

@@ -14,12 +14,15 @@
 // barrier, so the pass runs in place and the output is in natural order.
 // Register need depends on n/G only, never on how many lines a CTA holds.
 //
-// Shared-memory layout: element e of a line lives at slot L(e), where L is
-// either the identity or an XOR swizzle of e's position inside its 128-byte
-// block by e's block index (L(e) = e ^ ((e >> SH) & MASK)).  Which one is
-// cheaper depends on the radix plan (stride-R stores of even radices
-// conflict without it; radix-15 first passes conflict with it); the host
-// planner simulates the bank traffic of both and picks per plan.
+// Shared-memory layout: between passes, element e of a line lives at slot
+// L(e), either the identity or an XOR swizzle of e's position inside its
+// 128-byte block by e's block index (L(e) = e ^ ((e >> SH) & MASK)); the
+// host planner simulates the bank traffic of both and picks per plan.  The
+// line is identity-laid at both ends of every transform: the first pass
+// reads j + r*n/R and the last pass writes j + r*Ns (both unit-stride across
+// the group, conflict-free), so whole lines can move with TMA bulk copies
+// and vector loads while the interior passes still avoid the stride-R
+// conflicts of the first pass's stores.
 //
 // Twiddles: one table entry w_{Ns R}^m per butterfly class, computed on the
 // host in double with exact integer angle reduction; powers in registers.
@@ -121,9 +124,13 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <typename T, int R, int KM, int DIR, class Grp, class Lay>
+struct LayoutId {
+  __device__ __forceinline__ int operator()(int e) const { return e; }
+};
+
+template <typename T, int R, int KM, int DIR, class Grp, class LayI, class LayO>
 __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, const cx<T>* __restrict__ tw,
-                                         const Grp& g, const Lay& lay) {
+                                         const Grp& g, const LayI& lay_in, const LayO& lay_out) {
   // Idle slots (j >= nb) recompute the last butterfly instead of skipping it:
   // conditionally-defined register arrays become loop-carried live ranges in
   // the caller's line loop and triple the register footprint.
@@ -132,7 +139,7 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
   for (int k = 0; k < KM; ++k) {
     const int j = min(g.rank + k * g.size(), nb - 1);
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[k][r] = x[lay(j + r * nb)];
+    for (int r = 0; r < R; ++r) v[k][r] = x[lay_in(j + r * nb)];
     if (Ns > 1) {
       // one table load per butterfly: w = w_{Ns R}^(j mod Ns); the powers
       // w^r by running product (<= 15 roundings, ~1e-6 relative in fp32)
@@ -155,7 +162,7 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
       const int m = j % Ns;
       const int base = (j - m) * R + m;
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[lay(base + r * Ns)] = v[k][r];
+      for (int r = 0; r < R; ++r) x[lay_out(base + r * Ns)] = v[k][r];
     }
   }
   g.sync();
@@ -165,7 +172,7 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
 template <typename T, int DIR, class Grp, class Lay>
 __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int Ns, int R,
                                               const cx<T>* __restrict__ tw, const cx<T>* __restrict__ wr,
-                                              const Grp g, const Lay lay) {
+                                              const Grp g, const Lay lay_in, const Lay lay_out) {
   const int nb = n / R;
   cx<T> in[kMaxGenericPrime], out[kMaxGenericPrime];
   const int j = g.rank;
@@ -173,7 +180,7 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
   if (act) {
     const int m = j % Ns;
     for (int r = 0; r < R; ++r) {
-      cx<T> a = x[lay(j + r * nb)];
+      cx<T> a = x[lay_in(j + r * nb)];
       if (Ns > 1 && r > 0) {
         cx<T> ww = ldg_cx(tw + m * (R - 1) + r - 1);
         if (DIR > 0) ww.y = -ww.y;
@@ -198,7 +205,7 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
   if (act) {
     const int m = j % Ns;
     const int base = (j - m) * R + m;
-    for (int r = 0; r < R; ++r) x[lay(base + r * Ns)] = out[r];
+    for (int r = 0; r < R; ++r) x[lay_out(base + r * Ns)] = out[r];
   }
   g.sync();
 }
@@ -208,22 +215,22 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
 // (inlining all cases into one body blows up live ranges and spills).
 template <typename T, int R, int DIR, class Grp, class Lay>
 __device__ __noinline__ void fft_pass_rt(cx<T>* __restrict__ x, int nb, int Ns, const cx<T>* __restrict__ tw,
-                                         const Grp g, const Lay lay) {
-  fft_pass<T, R, KmOf<R, MaxElems<T>::value>::value, DIR>(x, nb, Ns, tw, g, lay);
+                                         const Grp g, const Lay lay_in, const Lay lay_out) {
+  fft_pass<T, R, KmOf<R, MaxElems<T>::value>::value, DIR>(x, nb, Ns, tw, g, lay_in, lay_out);
 }
 
-template <typename T, int DIR, class Grp, class Lay>
-__device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
-                                            const Lay& lay) {
+template <typename T, int DIR, class Grp>
+__device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g) {
   int Ns = 1;
   for (int p = 0; p < P.npass; ++p) {
     const int R = P.radix[p];
     const int nb = P.n / R;
     const cx<T>* tw = P.tw + P.tw_off[p];
+    const LayoutRt<T> lay_in{p == 0 ? 0 : P.laymask}, lay_out{p == P.npass - 1 ? 0 : P.laymask};
     switch (R) {
 #define ILS_FFT_CASE(RR)                            \
   case RR:                                          \
-    fft_pass_rt<T, RR, DIR>(x, nb, Ns, tw, g, lay); \
+    fft_pass_rt<T, RR, DIR>(x, nb, Ns, tw, g, lay_in, lay_out); \
     break;
       ILS_FFT_CASE(2)
       ILS_FFT_CASE(3)
@@ -241,7 +248,7 @@ __device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<
       ILS_FFT_CASE(16)
 #undef ILS_FFT_CASE
       default:
-        fft_pass_generic<T, DIR>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g, lay);
+        fft_pass_generic<T, DIR>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g, lay_in, lay_out);
         break;
     }
     Ns *= R;
@@ -255,12 +262,6 @@ __device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<
 struct FftRt {
   static constexpr int n = 0;
   static constexpr int G = 0;
-  template <typename T>
-  using Layout = LayoutRt<T>;
-  template <typename T>
-  __device__ static Layout<T> layout(const FftDev<T>& P) {
-    return Layout<T>{P.laymask};
-  }
 };
 template <int SWZ, int GG, int N, int... Rs>
 struct FftCt {
@@ -269,26 +270,43 @@ struct FftCt {
   static constexpr int swz = SWZ;
   static constexpr int npass = sizeof...(Rs);
   static_assert((Rs * ... * 1) == N, "radix product must equal N");
-  template <typename T>
-  using Layout = LayoutCt<T, SWZ ? kSwzMask<T> : 0>;
-  template <typename T>
-  __device__ static Layout<T> layout(const FftDev<T>&) {
-    return Layout<T>{};
+};
+
+template <int... Rs>
+struct RadixList {
+  static constexpr int r[sizeof...(Rs)] = {Rs...};
+  static constexpr int ns(int p) {  // product of the radices before pass p
+    int v = 1;
+    for (int q = 0; q < p; ++q) v *= r[q];
+    return v;
   }
 };
 
-template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, class Lay>
-__device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Lay& lay,
-                                            FftCt<SWZ, GG, N, Rs...>) {
+template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, int... Is>
+__device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
+                                                 std::integer_sequence<int, Is...>) {
   constexpr int ME = MaxElems<T>::value;
-  int Ns = 1, p = 0;
-  ((fft_pass<T, Rs, KmOf<Rs, ME>::value, DIR>(x, N / Rs, Ns, P.tw + P.tw_off[p], g, lay), Ns *= Rs, ++p), ...);
+  using RL = RadixList<Rs...>;
+  constexpr int NP = sizeof...(Rs);
+  using LaySw = LayoutCt<T, SWZ ? kSwzMask<T> : 0>;
+  (fft_pass<T, RL::r[Is], KmOf<RL::r[Is], ME>::value, DIR>(
+       x, N / RL::r[Is], RL::ns(Is), P.tw + P.tw_off[Is], g,
+       std::conditional_t<Is == 0, LayoutId, LaySw>{}, std::conditional_t<Is == NP - 1, LayoutId, LaySw>{}),
+   ...);
 }
 
-template <typename T, int DIR, class S, class Grp, class Lay>
-__device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Lay& lay) {
-  if constexpr (S::n == 0) fft_line_rt<T, DIR>(x, P, g, lay);
-  else fft_line_ct<T, DIR>(x, P, g, lay, S{});
+template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp>
+__device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
+                                            FftCt<SWZ, GG, N, Rs...>) {
+  fft_line_ct_impl<T, DIR, SWZ, GG, N, Rs...>(x, P, g, std::make_integer_sequence<int, sizeof...(Rs)>{});
+}
+
+// Full transform of one identity-laid line (DIR = -1 forward, +1 inverse,
+// unnormalised).  Every thread of the group must call it.
+template <typename T, int DIR, class S, class Grp>
+__device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g) {
+  if constexpr (S::n == 0) fft_line_rt<T, DIR>(x, P, g);
+  else fft_line_ct<T, DIR>(x, P, g, S{});
 }
 
 }  // namespace ils

@@ -32,6 +32,7 @@ enum RowMode : int {
 enum ColMode : int { COL_SOLVE = 0, COL_FWD = 1, COL_INV = 2 };
 
 constexpr int kStatusClean = 0x7f7f7f7f;  // cudaMemset(0x7f) pattern
+constexpr int kMaxBandLines = 32;        // band + 2 halo lines per row CTA (mbarriers)
 
 template <typename T>
 struct PenaltyDev {
@@ -135,43 +136,51 @@ __device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(
 __device__ __forceinline__ double fast_div(double a, double b) { return a / b; }
 
 // ------------------------------------------------------------ line access
-// Line i of a row CTA starts at lines + i*LP (complex slots, layout Lay).
-// In a packed line, real sample x lives in complex element x>>1, component
-// x&1; element pairs (2q, 2q+1) stay adjacent under either layout.
-template <typename T, bool PACKED, class Lay>
+// Line i of a row CTA starts at lines + i*LP (complex slots).  Outside the
+// FFT passes lines are identity-laid: in a packed line real sample x is the
+// x-th scalar of the line.
+template <typename T, bool PACKED>
 struct Lines {
   cx<T>* base;
   int LP;
-  Lay lay;
   __device__ __forceinline__ cx<T>* line(int i) const { return base + (size_t)i * LP; }
   __device__ __forceinline__ T get(int i, int x) const {
-    if (PACKED) return reinterpret_cast<const T*>(line(i))[2 * lay(x >> 1) + (x & 1)];
-    return line(i)[lay(x)].x;
+    if (PACKED) return reinterpret_cast<const T*>(line(i))[x];
+    return line(i)[x].x;
   }
   __device__ __forceinline__ void set(int i, int x, T v) const {
-    if (PACKED) reinterpret_cast<T*>(line(i))[2 * lay(x >> 1) + (x & 1)] = v;
-    else line(i)[lay(x)] = cx<T>{v, T(0)};
+    if (PACKED) reinterpret_cast<T*>(line(i))[x] = v;
+    else line(i)[x] = cx<T>{v, T(0)};
   }
-  // QW consecutive reals from x0 (QW | x0, packed lines): complex elements
-  // x0/2 .. x0/2 + QW/2 - 1 share one 128-byte block, so their slots are
-  // lay(x0/2) ^ q -- one index computation per strip.
+  // QW consecutive reals from x0 (QW | x0) of a packed line: vector loads
   template <int QW>
   __device__ __forceinline__ void get_strip(int i, int x0, T (&v)[QW]) const {
-    const cx<T>* z = line(i);
-    const int s = lay(x0 >> 1);
+    const T* z = reinterpret_cast<const T*>(line(i)) + x0;
+    if constexpr (sizeof(T) == 4 && QW % 4 == 0) {
 #pragma unroll
-    for (int q = 0; q < QW / 2; ++q) {
-      const cx<T> c = z[s ^ q];
-      v[2 * q] = c.x;
-      v[2 * q + 1] = c.y;
+      for (int q = 0; q < QW; q += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(z + q);
+        v[q] = a.x;
+        v[q + 1] = a.y;
+        v[q + 2] = a.z;
+        v[q + 3] = a.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < QW; ++q) v[q] = z[q];
     }
   }
   template <int QW>
   __device__ __forceinline__ void set_strip(int i, int x0, const T (&v)[QW]) const {
-    cx<T>* z = line(i);
-    const int s = lay(x0 >> 1);
+    T* z = reinterpret_cast<T*>(line(i)) + x0;
+    if constexpr (sizeof(T) == 4 && QW % 4 == 0) {
 #pragma unroll
-    for (int q = 0; q < QW / 2; ++q) z[s ^ q] = cx<T>{v[2 * q], v[2 * q + 1]};
+      for (int q = 0; q < QW; q += 4)
+        *reinterpret_cast<float4*>(z + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < QW; ++q) z[q] = v[q];
+    }
   }
 };
 
@@ -206,26 +215,69 @@ __device__ __forceinline__ void cp_async_wait_keep(int keep) {
   }
 }
 
+// ------------------------------------------------------------ TMA bulk copies
+// 1-D bulk copies (cp.async.bulk, SASS UBLKCP) of whole rows between global
+// memory and shared memory, completion tracked by an mbarrier (loads) or a
+// bulk group (stores).  16-byte aligned addresses, sizes multiple of 16.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy smem writes -> async proxy
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_reads() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------ real <-> half-complex packing
 // Forward post-process of one packed line: Z = FFT_N(x[2n] + i x[2n+1]) ->
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
 // O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
-template <typename T, class Grp, class Lay>
-__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g,
-                                         const Lay& lay) {
+template <typename T, class Grp>
+__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g) {
   for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
-      const cx<T> z0 = z[lay(0)];
-      z[lay(0)] = cx<T>{z0.x + z0.y, T(0)};
-      z[lay(N)] = cx<T>{z0.x - z0.y, T(0)};
+      const cx<T> z0 = z[0];
+      z[0] = cx<T>{z0.x + z0.y, T(0)};
+      z[N] = cx<T>{z0.x - z0.y, T(0)};
     } else {
-      const cx<T> zk = z[lay(k)], zm = z[lay(N - k)];
+      const cx<T> zk = z[k], zm = z[N - k];
       const cx<T> E{T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y)};
       const cx<T> d{T(0.5) * (zk.x - zm.x), T(0.5) * (zk.y + zm.y)};  // (zk - conj zm)/2
       const cx<T> O{d.y, -d.x};                                          // -i * d
       const cx<T> wO = cmul(ldg_cx(wreal + k), O);
-      z[lay(k)] = E + wO;
-      if (N - k != k) z[lay(N - k)] = conj(E - wO);
+      z[k] = E + wO;
+      if (N - k != k) z[N - k] = conj(E - wO);
     }
   }
   g.sync();
@@ -234,20 +286,19 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restric
 // Inverse pre-process: Z_k = E + iO, Z_{N-k} = conj(E) + i conj(O) with
 // E = X_k + conj X_{N-k}, O = (X_k - conj X_{N-k}) conj(w^k).  An inverse
 // N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
-template <typename T, class Grp, class Lay>
-__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g,
-                                        const Lay& lay) {
+template <typename T, class Grp>
+__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g) {
   for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
-      const T a = z[lay(0)].x, c = z[lay(N)].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
-      z[lay(0)] = cx<T>{a + c, a - c};
+      const T a = z[0].x, c = z[N].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
+      z[0] = cx<T>{a + c, a - c};
     } else {
-      const cx<T> xk = z[lay(k)], xm = z[lay(N - k)];
+      const cx<T> xk = z[k], xm = z[N - k];
       const cx<T> E{xk.x + xm.x, xk.y - xm.y};
       const cx<T> D{xk.x - xm.x, xk.y + xm.y};
       const cx<T> O = cmulc(D, ldg_cx(wreal + k));
-      z[lay(k)] = cx<T>{E.x - O.y, E.y + O.x};
-      if (N - k != k) z[lay(N - k)] = cx<T>{E.x + O.y, -E.y + O.x};
+      z[k] = cx<T>{E.x - O.y, E.y + O.x};
+      if (N - k != k) z[N - k] = cx<T>{E.x + O.y, -E.y + O.x};
     }
   }
   g.sync();
@@ -259,20 +310,27 @@ constexpr int kColThreads = 256;
 constexpr int kNarrowMaxW = 4 * 4 * kRowThreads;  // stencil: 4 strips x 4 columns per thread
 constexpr int kWideMaxW = 4 * 8 * kRowThreads;
 
+// Whole-row TMA bulk copies need 16-byte granularity: compile-time plans of
+// widths W = 2n with W % 8 == 0 (f / u rows of W*4 bytes, spectrum rows of
+// round16((n+1)*8) bytes inside 32-byte aligned, 4-element padded rows).
+template <typename T, class FS>
+constexpr bool kBulkRows = sizeof(T) == 4 && FS::n > 0 && (2 * FS::n) % 8 == 0;
+
 // SMODE >= 0: kernel specialised for that mode without trace (the hot
 // kernels; dead phases compiled out keeps the code inside the I-cache);
 // SMODE = -1: any mode from A.mode, optional energy trace.
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[32];
+  __shared__ unsigned long long bars[kMaxBandLines];
   using Grp = GroupT<FS::G>;
+  constexpr bool BULK = kBulkRows<T, FS> && PACKED;
   const int MODE = SMODE >= 0 ? SMODE : A.mode;  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = FS::G > 0 ? FS::G : A.fft.G;
   const Grp g{tid / G, G, tid % G};
   const int ngroups = nthr / G;
-  const auto lay = FS::template layout<T>(A.fft);
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * A.band;
   const int nb = min(A.band, A.H - r0);
@@ -282,9 +340,10 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   const int nl = halo ? nb + 2 : nb;
   const int y0 = halo ? r0 - 1 : r0;
   const int off = halo ? 1 : 0;
-  const Lines<T, PACKED, decltype(lay)> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP, lay};
+  const Lines<T, PACKED> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP};
   const PenaltyDev<T>& P = A.pen;
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
+  const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
 
   if (MODE == MODE_IT && tid < nb && (W * sizeof(T)) % 16 == 0 && (A.f_rp * sizeof(T)) % 16 == 0) {
     // the stencil reads f one row at a time: pull the band's rows into L2 now
@@ -327,21 +386,34 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     }
   } else {
     // ---------------- phase A: u rows into shared memory (group per line)
-    // Every group first issues asynchronous copies for all of its lines (one
-    // cp.async group per line), then transforms them in order while later
-    // lines are still in flight.
+    // Rows arrive asynchronously: one TMA bulk copy per row (compile-time
+    // plans) or per-element cp.async (runtime plans), issued for every line
+    // up front; each group then transforms its lines while later ones land.
     const int mine = (nl - g.id + ngroups - 1) / ngroups;  // lines owned by this group
-    const bool async_in = (MODE != MODE_F0) || PACKED;
-    if (async_in) {
+    if constexpr (BULK) {
+      if (tid == 0) {
+        for (int i = 0; i < nl; ++i) mbar_init(&bars[i], 1);
+        mbar_fence_init();
+        for (int i = 0; i < nl; ++i) {
+          const int y = wrapi(y0 + i, H);
+          const void* src = MODE == MODE_F0 ? (const void*)(fpl + (size_t)y * A.f_rp)
+                                            : (const void*)(A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp);
+          const unsigned bytes = MODE == MODE_F0 ? (unsigned)(W * sizeof(T)) : spec_bytes;
+          mbar_expect_tx(&bars[i], bytes);
+          bulk_g2s(L.line(i), src, bytes, &bars[i]);
+        }
+      }
+      __syncthreads();
+    } else if (MODE != MODE_F0 || PACKED) {
       for (int i = g.id; i < nl; i += ngroups) {
         const int y = wrapi(y0 + i, H);
         cx<T>* z = L.line(i);
         if (MODE == MODE_F0) {
           const cx<T>* src = reinterpret_cast<const cx<T>*>(fpl + (size_t)y * A.f_rp);
-          for (int q = g.rank; q < W / 2; q += g.size()) cp_async<sizeof(cx<T>)>(z + lay(q), src + q);
+          for (int q = g.rank; q < W / 2; q += g.size()) cp_async<sizeof(cx<T>)>(z + q, src + q);
         } else {
           const cx<T>* src = A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp;
-          for (int k = g.rank; k < A.Wc; k += g.size()) cp_async<sizeof(cx<T>)>(z + lay(k), src + k);
+          for (int k = g.rank; k < A.Wc; k += g.size()) cp_async<sizeof(cx<T>)>(z + k, src + k);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
@@ -351,8 +423,9 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     for (int i = g.id; i < nl; i += ngroups, ++li) {
       const int y = wrapi(y0 + i, H);
       cx<T>* z = L.line(i);
-      const bool own = i >= off && i < off + nb;
-      if (async_in) {
+      if constexpr (BULK) {
+        mbar_wait(&bars[i], 0);
+      } else if (MODE != MODE_F0 || PACKED) {
         cp_async_wait_keep(mine - 1 - li);
         g.sync();
       }
@@ -361,16 +434,15 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
         if (PACKED) {
-          c2r_pre<T>(z, A.N, A.wreal, g, lay);
+          c2r_pre<T>(z, A.N, A.wreal, g);
         } else {
           // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
-          for (int k = A.Wc + g.rank; k < W; k += g.size()) z[lay(k)] = conj(z[lay(W - k)]);
-          if (g.rank == 0) z[lay(0)].y = T(0);
+          for (int k = A.Wc + g.rank; k < W; k += g.size()) z[k] = conj(z[W - k]);
+          if (g.rank == 0) z[0].y = T(0);
           g.sync();
         }
-        fft_line<T, +1, FS>(z, A.fft, g, lay);
+        fft_line<T, +1, FS>(z, A.fft, g);
       }
-      (void)own;
     }
     __syncthreads();
 
@@ -379,17 +451,26 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
       double e = 0.0;
       T* upl = A.u + (size_t)b * A.u_ps;
       if (PACKED && !trace) {
-        const int np = W / 2;
+        // finiteness (smoother.py:166-167): fma(x, 0, c) is NaN iff some x is not finite
+        T chk = T(0);
         for (int j = 0; j < nb; ++j) {
-          cx<T>* dst = reinterpret_cast<cx<T>*>(upl + (size_t)(r0 + j) * A.u_rp);
-          const cx<T>* z = L.line(j + off);
-          for (int q = tid; q < np; q += nthr) {
-            const cx<T> v = z[lay(q)];
-            bad |= !(finite_(v.x) && finite_(v.y));
-            dst[q] = v;
+          const T* z = reinterpret_cast<const T*>(L.line(j + off));
+          for (int x = tid; x < W; x += nthr) chk = fma_rn(z[x], T(0), chk);
+        }
+        if constexpr (BULK) {
+          __syncthreads();
+          if (tid < nb) bulk_s2g(upl + (size_t)(r0 + tid) * A.u_rp, L.line(tid + off), (unsigned)(W * sizeof(T)));
+        } else {
+          const int np = W / 2;
+          for (int j = 0; j < nb; ++j) {
+            cx<T>* dst = reinterpret_cast<cx<T>*>(upl + (size_t)(r0 + j) * A.u_rp);
+            const cx<T>* z = L.line(j + off);
+            for (int q = tid; q < np; q += nthr) dst[q] = z[q];
           }
         }
+        bad = !finite_(chk);
         if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, A.iter);
+        if constexpr (BULK) bulk_wait_reads();
         return;
       }
       for (int t = tid; t < nb * W; t += nthr) {
@@ -527,21 +608,17 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
   // ---------------- phase C: r2c of rhs rows -> S_out (group per line)
   for (int i = g.id; i < nb; i += ngroups) {
     cx<T>* z = L.line(i);
-    fft_line<T, -1, FS>(z, A.fft, g, lay);
-    if (PACKED) r2c_post<T>(z, A.N, A.wreal, g, lay);
+    fft_line<T, -1, FS>(z, A.fft, g);
+    if (PACKED) r2c_post<T>(z, A.N, A.wreal, g);
+    else g.sync();
     cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
-    if (PACKED && sizeof(T) == 4) {
-      // 16-byte stores of element pairs (rows are 32-byte aligned)
-      for (int m = g.rank; 2 * m + 1 < A.Wc; m += g.size()) {
-        const int s = lay(2 * m);
-        const cx<T> a0 = z[s], a1 = z[s ^ 1];
-        reinterpret_cast<float4*>(dst)[m] = make_float4(a0.x, a0.y, a1.x, a1.y);
-      }
-      if ((A.Wc & 1) && g.rank == 0) dst[A.Wc - 1] = z[lay(A.Wc - 1)];
+    if constexpr (BULK) {
+      if (g.rank == 0) bulk_s2g(dst, z, spec_bytes);
     } else {
-      for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[lay(k)];
+      for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[k];
     }
   }
+  if constexpr (BULK) bulk_wait_reads();
 }
 
 // ------------------------------------------------------------ column pass
@@ -558,7 +635,6 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
   const int G = FS::G > 0 ? FS::G : A.fft.G;
   const Grp g{tid / G, G, tid % G};
   const int ngroups = nthr / G;
-  const auto lay = FS::template layout<T>(A.fft);
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * A.C;
   const int nc = min(A.C, A.Wc - c0);
@@ -568,32 +644,32 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
   const int ystep = nthr / nc, cc = tid % nc, y0 = tid / nc;
   const bool copier = tid < ystep * nc;
   if (copier)
-    for (int y = y0; y < H; y += ystep) cp_async<sizeof(cx<T>)>(tile + cc * A.CS + lay(y), Spl + (size_t)y * A.S_rp + cc);
+    for (int y = y0; y < H; y += ystep) cp_async<sizeof(cx<T>)>(tile + cc * A.CS + y, Spl + (size_t)y * A.S_rp + cc);
   if (A.mode == COL_SOLVE)
     for (int y = tid; y < H; y += nthr) swy[y] = __ldg(A.wy + y);
   cp_async_wait_all();
   __syncthreads();
   for (int c = g.id; c < nc; c += ngroups) {
     cx<T>* z = tile + c * A.CS;
-    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g, lay);
+    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g);
     if (A.mode == COL_SOLVE) {
       // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses
       const T base = T(1) + A.cl2 * __ldg(A.wx + c0 + c);
 #pragma unroll 4
       for (int y = g.rank; y < H; y += g.size()) {
         const T d = base + A.cl2 * swy[y];
-        z[lay(y)] = scale(z[lay(y)], fast_div(A.inv_hw, d));
+        z[y] = scale(z[y], fast_div(A.inv_hw, d));
       }
       g.sync();
     } else if (A.mode == COL_INV) {
-      for (int y = g.rank; y < H; y += g.size()) z[lay(y)] = scale(z[lay(y)], A.inv_hw);
+      for (int y = g.rank; y < H; y += g.size()) z[y] = scale(z[y], A.inv_hw);
       g.sync();
     }
-    if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g, lay);
+    if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g);
   }
   __syncthreads();
   if (copier)
-    for (int y = y0; y < H; y += ystep) Spl[(size_t)y * A.S_rp + cc] = tile[cc * A.CS + lay(y)];
+    for (int y = y0; y < H; y += ystep) Spl[(size_t)y * A.S_rp + cc] = tile[cc * A.CS + y];
 }
 
 // ------------------------------------------------------------ small kernels
