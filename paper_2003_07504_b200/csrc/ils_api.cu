@@ -122,9 +122,13 @@ const SpecHost kColSpecs[] = {ILS_COL_SPECS(ILS_HOST_SPEC)};
 // ideal, for a line layout (identity or XOR swizzle), following exactly the
 // index pattern of fft_pass.  E = complex elements per 128 B (16 fp32, 8 fp64);
 // a warp's request is served in phases of E lanes.
-double bank_cost(int n, const std::vector<int>& radix, int G, bool swz, int E, int maxe) {
+double bank_cost(int n, const std::vector<int>& radix, int G, int kind, int E, int maxe) {
   const int sh = E == 16 ? 4 : 3;
-  auto lay = [&](int e) { return swz ? (e ^ ((e >> sh) & (E - 1))) : e; };
+  auto lay = [&](int e) {
+    if (kind == 0) return e;
+    const int s = kind == 1 ? (e >> sh) : (e >> sh) ^ (e >> (sh + 1));
+    return e ^ (s & (E - 1));
+  };
   auto wave = [&](const int* addr, const bool* act, int lanes, double& tot, double& ideal) {
     for (int p0 = 0; p0 < lanes; p0 += E) {
       int cnt[16] = {0};
@@ -153,7 +157,7 @@ double bank_cost(int n, const std::vector<int>& radix, int G, bool swz, int E, i
     // lines are identity-laid at both ends of the transform (ils_fft.cuh)
     auto lay_in = [&](int e) { return pi == 0 ? e : lay(e); };
     auto lay_out = [&](int e) { return pi == np - 1 ? e : lay(e); };
-    const int nb = n / R, km = R <= 16 ? std::max(1, maxe / R) : 1;
+    const int nb = n / R, km = std::max(1, maxe / R);
     for (int k = 0; k < km; ++k)
       for (int w0 = 0; w0 < G; w0 += 32) {
         int ld[32], st[32];
@@ -200,13 +204,20 @@ bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
       }
     }
     if (!ok) return false;
-    out.swz = bank_cost(n, out.radix, out.G, true, E, maxe) < bank_cost(n, out.radix, out.G, false, E, maxe);
+    double best = 1e300;
+    for (int kind = 0; kind < 3; ++kind) {
+      const double c = bank_cost(n, out.radix, out.G, kind, E, maxe);
+      if (c < best - 1e-9) {
+        best = c;
+        out.swz = kind;
+      }
+    }
   }
   if ((int)out.radix.size() > kMaxPass) return false;
   long long Ns = 1;
   for (int R : out.radix) {
     out.tw_off.push_back((int)(out.tw.size() / 2));
-    if (R <= 16) {  // unrolled radices: w^m only, powers formed in registers
+    if (R <= 16 || spec) {  // unrolled radices: w^m only, powers formed in registers
       for (long long m = 0; m < Ns; ++m) {
         const sc_t w = sincos2pi(-m, Ns * R);
         out.tw.push_back(w.c);
@@ -221,7 +232,7 @@ bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
         }
     }
     out.gen_off.push_back((int)(out.tw.size() / 2));
-    if (R > 16)
+    if (R > 16 && !spec)
       for (int q = 0; q < R; ++q) {
         const sc_t w = sincos2pi(-q, R);
         out.tw.push_back(w.c);
@@ -374,7 +385,7 @@ template <typename T>
 void fill_fft_dev(FftDev<T>& d, const FftHost& h, const void* base, size_t off) {
   d.n = h.n;
   d.G = h.G;
-  d.laymask = h.swz ? (sizeof(T) == 4 ? 15 : 7) : 0;
+  d.laykind = h.swz;
   d.npass = (int)h.radix.size();
   for (int i = 0; i < kMaxPass; ++i) {
     d.radix[i] = i < d.npass ? h.radix[i] : 1;

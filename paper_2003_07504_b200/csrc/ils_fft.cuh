@@ -42,7 +42,7 @@ struct FftDev {
   int n;
   int npass;
   int G;        // threads per line group
-  int laymask;  // swizzle mask of the line layout (0 = identity)
+  int laykind;  // interior-pass line layout (0 identity, 1/2 XOR swizzles)
   int radix[kMaxPass];
   int tw_off[kMaxPass];   // pass twiddles: R<=16: Ns entries w^m; generic R: Ns*(R-1), [m][r-1]
   int gen_off[kMaxPass];  // generic primes: R entries w_R^q
@@ -57,15 +57,26 @@ struct SwzShift {
 template <typename T>
 constexpr int kSwzMask = (1 << SwzShift<T>::value) - 1;
 
-// Line layouts.  LayoutCt: compile-time mask (hot sizes); LayoutRt: runtime.
-template <typename T, int MASK>
+// Line layouts: kind 0 identity, 1 XOR by the 128-byte block index, 2 XOR
+// by (block index ^ block index >> 1) -- the latter suits radix-32 first
+// passes.  LayoutCt: compile-time kind (hot sizes); LayoutRt: runtime.
+template <typename T, int KIND>
 struct LayoutCt {
-  __device__ __forceinline__ int operator()(int e) const { return e ^ ((e >> SwzShift<T>::value) & MASK); }
+  __device__ __forceinline__ int operator()(int e) const {
+    constexpr int SH = SwzShift<T>::value, M = kSwzMask<T>;
+    if constexpr (KIND == 0) return e;
+    else if constexpr (KIND == 1) return e ^ ((e >> SH) & M);
+    else return e ^ (((e >> SH) ^ (e >> (SH + 1))) & M);
+  }
 };
 template <typename T>
 struct LayoutRt {
-  int mask;
-  __device__ __forceinline__ int operator()(int e) const { return e ^ ((e >> SwzShift<T>::value) & mask); }
+  int kind;
+  __device__ __forceinline__ int operator()(int e) const {
+    constexpr int SH = SwzShift<T>::value, M = kSwzMask<T>;
+    const int s = kind == 1 ? (e >> SH) : (e >> SH) ^ (e >> (SH + 1));
+    return kind == 0 ? e : e ^ (s & M);
+  }
 };
 
 template <typename T>
@@ -142,14 +153,34 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
     for (int r = 0; r < R; ++r) v[k][r] = x[lay_in(j + r * nb)];
     if (Ns > 1) {
       // one table load per butterfly: w = w_{Ns R}^(j mod Ns); the powers
-      // w^r by running product (<= 15 roundings, ~1e-6 relative in fp32)
+      // w^r by running product (<= 15 roundings) for R <= 16, and for larger
+      // radices w^(8a+b) = (w^8)^a w^b (two short chains instead of one long)
       cx<T> w1 = ldtw(tw + (j % Ns));
       if (DIR > 0) w1.y = -w1.y;
-      cx<T> w = w1;
+      if constexpr (R <= 16) {
+        cx<T> w = w1;
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        v[k][r] = cmul(v[k][r], w);
-        if (r + 1 < R) w = cmul(w, w1);
+        for (int r = 1; r < R; ++r) {
+          v[k][r] = cmul(v[k][r], w);
+          if (r + 1 < R) w = cmul(w, w1);
+        }
+      } else {
+        cx<T> wb[8];
+        wb[1] = w1;
+#pragma unroll
+        for (int b = 2; b < 8; ++b) wb[b] = cmul(wb[b - 1], w1);
+        const cx<T> w8 = cmul(wb[4], wb[4]);
+        cx<T> wa = w8;
+#pragma unroll
+        for (int a = 0; a * 8 < R; ++a) {
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const int r = 8 * a + b;
+            if (r == 0 || r >= R) continue;
+            v[k][r] = cmul(v[k][r], a == 0 ? wb[b] : (b == 0 ? wa : cmul(wa, wb[b])));
+          }
+          if (a > 0) wa = cmul(wa, w8);
+        }
       }
     }
     dft<R, DIR>(v[k]);
@@ -226,7 +257,7 @@ __device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<
     const int R = P.radix[p];
     const int nb = P.n / R;
     const cx<T>* tw = P.tw + P.tw_off[p];
-    const LayoutRt<T> lay_in{p == 0 ? 0 : P.laymask}, lay_out{p == P.npass - 1 ? 0 : P.laymask};
+    const LayoutRt<T> lay_in{p == 0 ? 0 : P.laykind}, lay_out{p == P.npass - 1 ? 0 : P.laykind};
     switch (R) {
 #define ILS_FFT_CASE(RR)                            \
   case RR:                                          \
@@ -288,7 +319,7 @@ __device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const Ff
   constexpr int ME = MaxElems<T>::value;
   using RL = RadixList<Rs...>;
   constexpr int NP = sizeof...(Rs);
-  using LaySw = LayoutCt<T, SWZ ? kSwzMask<T> : 0>;
+  using LaySw = LayoutCt<T, SWZ>;
   (fft_pass<T, RL::r[Is], KmOf<RL::r[Is], ME>::value, DIR>(
        x, N / RL::r[Is], RL::ns(Is), P.tw + P.tw_off[Is], g,
        std::conditional_t<Is == 0, LayoutId, LaySw>{}, std::conditional_t<Is == NP - 1, LayoutId, LaySw>{}),

@@ -711,7 +711,7 @@ __global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long n
 // runtime-planned path (FftRt).  The host planner (ils_api.cu) uses exactly
 // these radix lists when n matches, so twiddle tables and kernels agree.
 // X(id, swizzle, group threads, n, radices...)
-#define ILS_ROW_SPECS(X) X(0, 1, 32, 256, 16, 16) X(1, 1, 64, 960, 16, 15, 4) X(2, 1, 128, 1920, 16, 15, 8) X(3, 1, 256, 3840, 16, 16, 15) X(4, 1, 32, 512, 16, 8, 4)
+#define ILS_ROW_SPECS(X) X(0, 1, 32, 256, 16, 16) X(1, 2, 32, 960, 32, 30) X(2, 1, 128, 1920, 16, 15, 8) X(3, 1, 256, 3840, 16, 16, 15) X(4, 1, 32, 512, 16, 8, 4)
 // row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
 #define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)
 #define ILS_COL_SPECS(X) X(0, 1, 32, 512, 16, 8, 4) X(1, 0, 128, 1080, 15, 9, 8) X(2, 1, 256, 2160, 16, 15, 9) X(3, 1, 32, 256, 16, 16) X(4, 1, 128, 720, 16, 9, 5)
