@@ -52,6 +52,15 @@ def bytes_per_frame(iters=ITERS, h=H, w=W, ch=CH):
     return ch * per_plane
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return float(json.load(fh)[kernel]["bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -106,14 +115,15 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_port_frame_seconds(frames=1, seed=20240607):
+def cpu_port_frame_seconds(frames=1, seed=20240607, warm=True):
     """Oracle port (the reference algorithm, numpy + scipy.fft) on one 1080p RGB frame."""
     from oracle import ils_oracle as O
 
     workers = os.cpu_count() or 1
     planes = O.bench_planes(H, W, CH, seed=seed)
     pen = O.Charbonnier(P_EXP, EPS)
-    O.smooth_color(planes[:1], pen, LAM, ITERS, workers=workers)  # warm-up (plans, pages)
+    if warm:
+        O.smooth_color(planes[:1], pen, LAM, ITERS, workers=workers)  # warm-up (plans, pages)
     t0 = time.perf_counter()
     for _ in range(frames):
         O.smooth_color(planes, pen, LAM, ITERS, workers=workers)
@@ -126,8 +136,10 @@ def run_reference(args, rank):
         return
     sec, workers = cpu_port_frame_seconds(frames=1)  # warm-up + one sample
     samples = []
-    for _ in range(max(1, args.steps)):
-        s, _ = cpu_port_frame_seconds(frames=1)
+    # each step is one 1080p RGB frame (~1 s on 16 cores): cap the sample so
+    # the reference arm finishes within a few minutes at any --steps
+    for _ in range(max(1, min(args.steps, 30))):
+        s, _ = cpu_port_frame_seconds(frames=1, warm=False)
         samples.append(s)
     mean = sum(samples) / len(samples)
     fps = 1.0 / mean
@@ -147,7 +159,7 @@ def run_reference(args, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--frames", type=int, default=16, help="frames per step per GPU")
     ap.add_argument("--group", type=int, default=1, help="frames per ils_smooth call (L2-resident group)")
@@ -314,7 +326,8 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": round(row_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(row_gbs / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                         "frac": round(row_gbs / peak, 4), "traffic": measured_traffic("k_row_it"),
+                         "traffic_source": "profiles/traffic.json (ncu --set full, warm L2)", "peak_kind": peak_kind,
                          "kernel": "k_row fused row pass (iteration>=1)", "ms": round(ms_row, 4),
                          "bytes_per_launch": row_bytes,
                          "col_pass": {"achieved": round(col_gbs, 1), "frac": round(col_gbs / peak, 4),
