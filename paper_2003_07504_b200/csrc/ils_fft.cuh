@@ -139,9 +139,19 @@ struct LayoutId {
   __device__ __forceinline__ int operator()(int e) const { return e; }
 };
 
-template <typename T, int R, int KM, int DIR, class Grp, class LayI, class LayO>
+// Pointwise map applied to elements as a transform's first pass loads them
+// (e.g. the column pass's 1/(H W denom) multiply, fused into the inverse).
+struct NoPre {
+  template <typename C>
+  __device__ __forceinline__ C operator()(int, C v) const {
+    return v;
+  }
+};
+
+template <typename T, int R, int KM, int DIR, class Grp, class LayI, class LayO, class Pre = NoPre>
 __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, const cx<T>* __restrict__ tw,
-                                         const Grp& g, const LayI& lay_in, const LayO& lay_out) {
+                                         const Grp& g, const LayI& lay_in, const LayO& lay_out,
+                                         const Pre& pre = Pre{}) {
   // Idle slots (j >= nb) recompute the last butterfly instead of skipping it:
   // conditionally-defined register arrays become loop-carried live ranges in
   // the caller's line loop and triple the register footprint.
@@ -150,7 +160,7 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
   for (int k = 0; k < KM; ++k) {
     const int j = min(g.rank + k * g.size(), nb - 1);
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[k][r] = x[lay_in(j + r * nb)];
+    for (int r = 0; r < R; ++r) v[k][r] = pre(j + r * nb, x[lay_in(j + r * nb)]);
     if (Ns > 1) {
       // one table load per butterfly: w = w_{Ns R}^(j mod Ns); the powers
       // w^r by running product (<= 15 roundings) for R <= 16, and for larger
@@ -286,6 +296,12 @@ __device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<
   }
 }
 
+template <bool FIRST, class Pre>
+__device__ __forceinline__ std::conditional_t<FIRST, Pre, NoPre> pick_pre(const Pre& p) {
+  if constexpr (FIRST) return p;
+  else return NoPre{};
+}
+
 // ------------------------------------------------------------ plans as types
 // FftRt: runtime plan (FftDev), runtime group size and layout.
 // FftCt<SWZ, G, N, radices...>: the hot sizes -- group size, layout, n, Ns
@@ -313,31 +329,40 @@ struct RadixList {
   }
 };
 
-template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, int... Is>
+template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, class Pre, int... Is>
 __device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
-                                                 std::integer_sequence<int, Is...>) {
+                                                 const Pre& pre, std::integer_sequence<int, Is...>) {
   constexpr int ME = MaxElems<T>::value;
   using RL = RadixList<Rs...>;
   constexpr int NP = sizeof...(Rs);
   using LaySw = LayoutCt<T, SWZ>;
   (fft_pass<T, RL::r[Is], KmOf<RL::r[Is], ME>::value, DIR>(
        x, N / RL::r[Is], RL::ns(Is), P.tw + P.tw_off[Is], g,
-       std::conditional_t<Is == 0, LayoutId, LaySw>{}, std::conditional_t<Is == NP - 1, LayoutId, LaySw>{}),
+       std::conditional_t<Is == 0, LayoutId, LaySw>{}, std::conditional_t<Is == NP - 1, LayoutId, LaySw>{},
+       std::conditional_t<Is == 0, Pre, NoPre>(pick_pre<Is == 0>(pre))),
    ...);
 }
 
-template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp>
-__device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
+template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, class Pre>
+__device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Pre& pre,
                                             FftCt<SWZ, GG, N, Rs...>) {
-  fft_line_ct_impl<T, DIR, SWZ, GG, N, Rs...>(x, P, g, std::make_integer_sequence<int, sizeof...(Rs)>{});
+  fft_line_ct_impl<T, DIR, SWZ, GG, N, Rs...>(x, P, g, pre, std::make_integer_sequence<int, sizeof...(Rs)>{});
 }
 
 // Full transform of one identity-laid line (DIR = -1 forward, +1 inverse,
 // unnormalised).  Every thread of the group must call it.
-template <typename T, int DIR, class S, class Grp>
-__device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g) {
-  if constexpr (S::n == 0) fft_line_rt<T, DIR>(x, P, g);
-  else fft_line_ct<T, DIR>(x, P, g, S{});
+template <typename T, int DIR, class S, class Grp, class Pre = NoPre>
+__device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
+                                         const Pre& pre = Pre{}) {
+  if constexpr (S::n == 0) {
+    if constexpr (!std::is_same<Pre, NoPre>::value) {  // runtime plans: apply the map as its own sweep
+      for (int e = g.rank; e < P.n; e += g.size()) x[e] = pre(e, x[e]);
+      g.sync();
+    }
+    fft_line_rt<T, DIR>(x, P, g);
+  } else {
+    fft_line_ct<T, DIR>(x, P, g, pre, S{});
+  }
 }
 
 }  // namespace ils

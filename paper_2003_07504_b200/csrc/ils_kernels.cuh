@@ -622,6 +622,20 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
 }
 
 // ------------------------------------------------------------ column pass
+template <typename T>
+struct DenomScale {  // v * inv_hw / (1 + c lam/2 (wx[kx] + wy[ky]))
+  const T* wy;
+  T base, cl2, inv_hw;
+  __device__ __forceinline__ cx<T> operator()(int y, cx<T> v) const {
+    return scale(v, fast_div(inv_hw, base + cl2 * wy[y]));
+  }
+};
+template <typename T>
+struct UniformScale {
+  T s;
+  __device__ __forceinline__ cx<T> operator()(int, cx<T> v) const { return scale(v, s); }
+};
+
 // A strip of C columns is loaded transposed into C lines (line pitch CS
 // chosen so the transposing copies are bank-conflict-free); a group owns one
 // column at a time: forward FFT, * 1/(H W denom), inverse FFT.
@@ -653,19 +667,15 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
     cx<T>* z = tile + c * A.CS;
     if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g);
     if (A.mode == COL_SOLVE) {
-      // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses
+      // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses,
+      // applied as the inverse transform's first pass loads each element
       const T base = T(1) + A.cl2 * __ldg(A.wx + c0 + c);
-#pragma unroll 4
-      for (int y = g.rank; y < H; y += g.size()) {
-        const T d = base + A.cl2 * swy[y];
-        z[y] = scale(z[y], fast_div(A.inv_hw, d));
-      }
-      g.sync();
+      const DenomScale<T> pre{swy, base, A.cl2, A.inv_hw};
+      fft_line<T, +1, FS>(z, A.fft, g, pre);
     } else if (A.mode == COL_INV) {
-      for (int y = g.rank; y < H; y += g.size()) z[y] = scale(z[y], A.inv_hw);
-      g.sync();
+      const UniformScale<T> pre{A.inv_hw};
+      fft_line<T, +1, FS>(z, A.fft, g, pre);
     }
-    if (A.mode != COL_FWD) fft_line<T, +1, FS>(z, A.fft, g);
   }
   __syncthreads();
   if (copier)
