@@ -3,8 +3,9 @@
 // Replaces the inner arithmetic of scipy.fft.fft2/ifft2 that the reference
 // calls through solver.py:24-30.  Everything here is compile-time shaped:
 // a radix-R DFT over R complex values held in registers, with every twiddle
-// a constexpr folded into the instruction stream.  Composite radices are
-// built by Cooley-Tukey from 2, 4 and odd primes (3, 5, 7, 11, 13).
+// a constexpr folded into the instruction stream.  Composite radices with
+// coprime factors use the prime-factor algorithm (no internal twiddles),
+// prime powers Cooley-Tukey from 2, 4 and odd primes (3, 5, 7, 11, 13).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -113,6 +114,27 @@ constexpr int ct_split() {
   return split_of(R);
 }
 
+constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
+constexpr int modinv_i(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
+  int r = 1;
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) r = x;
+  return r;
+}
+// Coprime split for the prime-factor (Good-Thomas) algorithm: the power-of-
+// two part of r, else the first odd prime power; 0 when r is a prime power.
+constexpr int pfa_split(int r) {
+  const int p2 = r & -r;
+  if (p2 > 1 && p2 < r) return p2;
+  for (int p = 3; p <= r; p += 2) {
+    if (r % p) continue;
+    int a = 1;
+    while (r % (a * p) == 0) a *= p;
+    return a < r ? a : 0;
+  }
+  return 0;
+}
+
 // Multiply by w = exp(DIR * 2*pi*i * K / R), specialised for quarter turns.
 template <int K, int R, int DIR, typename T>
 __device__ __forceinline__ cx<T> twc(cx<T> a) {
@@ -191,6 +213,28 @@ __device__ __forceinline__ void dft_ct(cx<T>* v) {
   sfor<R>([&](auto I) { v[ILS_CV(I)] = o[ILS_CV(I)]; });
 }
 
+// Prime-factor algorithm, R = A*B with gcd(A, B) = 1: no internal twiddles.
+// n = (n1 B + n2 A) mod R, k = (k1 B (B^-1 mod A) + k2 A (A^-1 mod B)) mod R.
+template <int R, int DIR, typename T>
+__device__ __forceinline__ void dft_pfa(cx<T>* v) {
+  constexpr int A = pfa_split(R), B = R / A;
+  constexpr int Ai = modinv_i(A % B, B), Bi = modinv_i(B % A, A);
+  cx<T> y[R];
+  sfor<B>([&](auto N2) {
+    constexpr int n2 = ILS_CV(N2);
+    cx<T> t[A];
+    sfor<A>([&](auto N1) { t[ILS_CV(N1)] = v[(ILS_CV(N1) * B + n2 * A) % R]; });
+    dft<A, DIR>(t);
+    sfor<A>([&](auto K1) { y[ILS_CV(K1) * B + n2] = t[ILS_CV(K1)]; });
+  });
+  sfor<A>([&](auto K1) { dft<B, DIR>(y + ILS_CV(K1) * B); });
+  sfor<A>([&](auto K1) {
+    sfor<B>([&](auto K2) {
+      v[(ILS_CV(K1) * B * Bi + ILS_CV(K2) * A * Ai) % R] = y[ILS_CV(K1) * B + ILS_CV(K2)];
+    });
+  });
+}
+
 // X[k] = sum_n v[n] exp(DIR * 2*pi*i*n*k/R), unnormalised, in place.
 template <int R, int DIR, typename T>
 __device__ __forceinline__ void dft(cx<T>* v) {
@@ -210,6 +254,8 @@ __device__ __forceinline__ void dft(cx<T>* v) {
     v[3] = a1 - a3;
   } else if constexpr (ct_is_prime<R>()) {
     dft_prime<R, DIR>(v);
+  } else if constexpr (pfa_split(R) > 0) {
+    dft_pfa<R, DIR>(v);
   } else {
     dft_ct<R, DIR>(v);
   }

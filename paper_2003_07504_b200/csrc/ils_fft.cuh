@@ -44,7 +44,7 @@ struct FftDev {
   int G;        // threads per line group
   int laykind;  // interior-pass line layout (0 identity, 1/2 XOR swizzles)
   int radix[kMaxPass];
-  int tw_off[kMaxPass];   // pass twiddles: R<=16: Ns entries w^m; generic R: Ns*(R-1), [m][r-1]
+  int tw_off[kMaxPass];   // pass twiddles: unrolled R: Ns entries w^m; generic R: Ns*(R-1), [m][r-1]
   int gen_off[kMaxPass];  // generic primes: R entries w_R^q
   const cx<T>* tw;
 };
@@ -164,7 +164,9 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
     if (Ns > 1) {
       // one table load per butterfly: w = w_{Ns R}^(j mod Ns); the powers
       // w^r by running product (<= 15 roundings) for R <= 16, and for larger
-      // radices w^(8a+b) = (w^8)^a w^b (two short chains instead of one long)
+      // radices w^(8a+b) = (w^8)^a w^b (two short chains instead of one long).
+      // Loading all R-1 powers measured slower (load latency on the critical
+      // path of every pass).
       cx<T> w1 = ldtw(tw + (j % Ns));
       if (DIR > 0) w1.y = -w1.y;
       if constexpr (R <= 16) {
