@@ -301,9 +301,9 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
     if (smem > 227 * 1024) break;
     const int per_sm = smem <= 113 * 1024 ? 2 : 1;
     const long ctas = (long)p.B * ((p.H + band - 1) / band);
-    const long slots = (long)p.sms * per_sm;
-    const double waves = (double)((ctas + slots - 1) / slots);
-    const double cost = waves * (2.0 * band + 2.0 + 0.5 * band) * (per_sm == 1 ? 2.0 : 1.0);
+    // issue-bound: time ~ the busiest SM's work (b+2 c2r, b r2c, b stencil rows)
+    const double per_sm_ctas = (double)((ctas + p.sms - 1) / p.sms);
+    const double cost = per_sm_ctas * (2.5 * band + 2.0) * (per_sm == 1 ? 1.5 : 1.0);
     if (cost < best * (1 - 1e-9)) {
       best = cost;
       p.band = band;
@@ -353,11 +353,12 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
     }
     const size_t smem = (size_t)C * bestCS * elt + (size_t)p.H * (elt / 2);  // tile + wy
     if (smem > 227 * 1024) break;
-    const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+    // resident CTAs/SM: k_col is register-bounded to 3 (launch bounds), smem to 228 KB
+    const int per_sm = (int)std::min<size_t>(kColMinBlocks, (228 * 1024) / (smem + 1024));
     const long strips = (p.Wc + C - 1) / C;
     const long ctas = (long)p.B * strips;
-    const long slots = (long)p.sms * per_sm;
-    const double waves = (double)((ctas + slots - 1) / slots);
+    // the pass is issue-bound: time ~ the busiest SM's column count
+    const double per_sm_ctas = (double)((ctas + p.sms - 1) / p.sms);
     // 32-byte sectors a strip's row segment touches (rows are 32 B aligned)
     double sectors = 0;
     for (long s = 0; s < strips; ++s) {
@@ -366,8 +367,7 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
     }
     sectors /= strips;
     const double col_sectors = (double)elt / 32.0;  // one column's share at perfect coalescing
-    const double cost =
-        waves * ((C + ngroups - 1) / ngroups + 0.5 * sectors / col_sectors) * (per_sm == 1 ? 2.0 : 1.0);
+    const double cost = per_sm_ctas * (C + 0.25 * (sectors / col_sectors - C) + 0.5) * (per_sm == 1 ? 1.5 : 1.0);
     if (cost < best * (1 - 1e-6) || (cost < best * (1 + 1e-6) && C > p.C)) {
       best = cost;
       p.C = C;

@@ -307,6 +307,7 @@ __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict
 // ------------------------------------------------------------ row pass
 constexpr int kRowThreads = 256;
 constexpr int kColThreads = 256;
+constexpr int kColMinBlocks = 3;  // k_col register budget: 3 CTAs / SM
 constexpr int kNarrowMaxW = 4 * 4 * kRowThreads;  // stencil: 4 strips x 4 columns per thread
 constexpr int kWideMaxW = 4 * 8 * kRowThreads;
 
@@ -640,7 +641,7 @@ struct UniformScale {
 // chosen so the transposing copies are bank-conflict-free); a group owns one
 // column at a time: forward FFT, * 1/(H W denom), inverse FFT.
 template <typename T, class FS>
-__global__ void __launch_bounds__(kColThreads, 2) k_col(const ColArgs<T> A) {
+__global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_col(const ColArgs<T> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
   T* swy = reinterpret_cast<T*>(tile + A.C * A.CS);  // wy[0..H) staged once per CTA
