@@ -124,6 +124,33 @@ ILS_API ils_status ils_irfft2(const ils_plan* plan, void* spec_dev, int64_t spec
 ILS_API ils_status ils_rgb_yuv(void* planes_dev, int32_t dtype, int64_t plane_stride, int64_t npx, int32_t frames,
                        int32_t inverse, void* stream);
 
+/* ---- C5: one image slab-decomposed over nranks GPUs --------
+ * Rank r owns rows [row0[r], row0[r+1]) for the row passes and spectrum
+ * columns [col0[r], col0[r+1]) for the column passes.  Between them the
+ * caller moves the half spectrum with two all-to-alls (NCCL on GPU):
+ *   forward  (row -> col): rank r sends peer q a block [H_r][pitch[q]];
+ *            it receives [H_q][pitch[r]] from every q, i.e. [H][pitch[r]];
+ *   reverse  (col -> row): rank r sends peer q its rows plus q's two halo
+ *            rows, [H_q + 2][pitch[r]] (periodic across ranks); it receives
+ *            [H_r + 2][pitch[q]] from every q.
+ * The kernels read and write those blocks directly (the pack/unpack of the
+ * transpose is fused into the row pass's loads/stores and the column pass's
+ * scatter).  ils_slab_get_layout returns row0/col0 (nranks+1 entries),
+ * pitch (nranks) and counts[4][8] in complex elements: fwd send, fwd recv,
+ * rev send, rev recv per peer.  f_ext is the rank's f rows plus the two
+ * halo rows [H_r + 2][width]; u is [H_r][width]. */
+ILS_API ils_status ils_slab_plan_create(ils_plan** out, int32_t height, int32_t width, const ils_params* params,
+                                        int32_t dtype, int32_t device, int32_t nranks, int32_t rank);
+ILS_API ils_status ils_slab_get_layout(const ils_plan* plan, int32_t* row0, int32_t* col0, int32_t* pitch,
+                                       int64_t* counts);
+/* mode 0: iteration-0 row pass (f_ext -> fwd send); 1: fused row pass
+ * (rev recv -> fwd send), `iter` = index of the iterate it reads; 3: final
+ * row pass (rev recv -> u). */
+ILS_API ils_status ils_slab_row_pass(const ils_plan* plan, int32_t mode, const void* f_ext, const void* rev_recv,
+                                     void* fwd_send, void* u, int32_t iter, void* stream, int32_t* status_dev);
+/* Column solve pass on this rank's columns: fwd recv -> rev send. */
+ILS_API ils_status ils_slab_col_pass(const ils_plan* plan, void* fwd_recv, void* rev_send, void* stream);
+
 /* Introspection for tests and the bench. */
 typedef struct {
   int32_t batch, height, width, dtype, packed;

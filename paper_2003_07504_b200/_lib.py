@@ -23,7 +23,8 @@ STATUS_CLEAN = 0x7F7F7F7F
 
 EXPORTS = (
     "ils_plan_create", "ils_plan_destroy", "ils_workspace_size", "ils_smooth", "ils_smooth_host",
-    "ils_host_io_size", "ils_launch_pass",
+    "ils_host_io_size", "ils_launch_pass", "ils_slab_plan_create", "ils_slab_get_layout", "ils_slab_row_pass",
+    "ils_slab_col_pass",
     "ils_solve_ls", "ils_rfft2", "ils_irfft2", "ils_rgb_yuv", "ils_plan_get_info", "ils_last_error",
     "ils_abi_version",
 )
@@ -68,6 +69,12 @@ _SIGS = {
     "ils_irfft2": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
     "ils_rgb_yuv": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P]),
     "ils_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
+    "ils_slab_plan_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, C.POINTER(Params), C.c_int32, C.c_int32,
+                                       C.c_int32, C.c_int32]),
+    "ils_slab_get_layout": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int64)]),
+    "ils_slab_row_pass": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P]),
+    "ils_slab_col_pass": (C.c_int, [_P, _P, _P, _P]),
     "ils_last_error": (C.c_char_p, []),
     "ils_abi_version": (C.c_int32, []),
 }

@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libils_b200.so")
 
 # (source, extra defines): ils_inst.cu is compiled once per kernel family
 N_ROW_SPECS = 5
-N_COL_SPECS = 5
+N_COL_SPECS = 6
 UNITS = ([("ils_api.cu", "api", [])]
          + [("ils_inst.cu", f"row_rt_{t}", [f"-DILS_INST_ROW_RT={t}"]) for t in ("float", "double")]
          + [("ils_inst.cu", f"col_rt_{t}", [f"-DILS_INST_COL_RT={t}"]) for t in ("float", "double")]

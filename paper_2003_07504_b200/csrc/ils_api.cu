@@ -50,9 +50,9 @@ const int kUnrolled[] = {16, 15, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2};
 // A group of G threads owns one n-point line; a radix-R pass gives each
 // thread ceil((n/R)/G) butterflies, which must fit its KM = MAXE/R slots
 // (generic primes: one butterfly per thread).
-bool pass_fits(int R, long long n, int G, int maxe) {
+bool pass_fits(int R, long long n, int G, int maxe, bool unrolled = false) {
   const long long tasks = n / R;
-  const int km = (R <= 16) ? std::max(1, maxe / R) : 1;
+  const int km = (R <= 16 || unrolled) ? std::max(1, maxe / R) : 1;  // KmOf<R, ME> (ils_fft.cuh)
   return (tasks + G - 1) / G <= km;
 }
 
@@ -110,10 +110,10 @@ bool has_big_prime(int n) {
 }
 
 struct SpecHost {
-  int id, swz, G, n;
+  int id, swz, G, me, n;
   std::vector<int> radix;
 };
-#define ILS_HOST_SPEC(ID, SWZ, GG, N, ...) SpecHost{ID, SWZ, GG, N, {__VA_ARGS__}},
+#define ILS_HOST_SPEC(ID, SWZ, GG, ME, N, ...) SpecHost{ID, SWZ, GG, ME, N, {__VA_ARGS__}},
 const SpecHost kRowSpecs[] = {ILS_ROW_SPECS(ILS_HOST_SPEC)};
 const SpecHost kColSpecs[] = {ILS_COL_SPECS(ILS_HOST_SPEC)};
 #undef ILS_HOST_SPEC
@@ -187,7 +187,7 @@ bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
   out.n = n;
   if (spec) {
     for (int R : spec->radix)
-      if (!pass_fits(R, n, spec->G, maxe)) return false;
+      if (!pass_fits(R, n, spec->G, spec->me, true)) return false;
     out.radix = spec->radix;
     out.G = spec->G;
     out.swz = spec->swz;
@@ -262,6 +262,11 @@ struct ils_plan {
   size_t off_rowtw, off_coltw, off_wreal, off_wx, off_wy, off_sink;  // byte offsets
   size_t spec_bytes;                                       // one half spectrum
   size_t epart_elems;                                      // doubles for trace partials
+  // slab decomposition (ils_slab_plan_create): this rank's rows / columns
+  bool slab = false;
+  int P = 1, rank = 0;
+  int row0[kMaxSeg + 1] = {0}, col0[kMaxSeg + 1] = {0}, pitch[kMaxSeg] = {0};
+  int Hl = 0, Wcl = 0;  // local rows, local spectrum columns
 };
 
 namespace {
@@ -419,6 +424,7 @@ PenaltyDev<T> pen_dev(const ils_params& q) {
 template <typename T>
 RowArgs<T> row_args(const ils_plan* p) {
   RowArgs<T> a{};
+  a.wrap = 1;
   a.B = p->B;
   a.H = p->H;
   a.W = p->W;
@@ -728,6 +734,7 @@ ils_status ils_smooth(const ils_plan* p, const void* f, void* u, int64_t ps, voi
                       double* energies) {
   if (!p || !f || !u || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (p->slab) return fail(ILS_EINVAL, "slab plans run through ils_slab_row_pass / ils_slab_col_pass");
   if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
@@ -934,6 +941,211 @@ ils_status ils_rgb_yuv(void* planes, int32_t dtype, int64_t ps, int64_t npx, int
     k_rgb_yuv<double><<<blocks, 256, 0, s>>>(static_cast<double*>(planes), ps, npx, frames, inverse);
   ILS_CUDA(cudaGetLastError());
   return ILS_OK;
+}
+
+// ------------------------------------------------------------ slab decomposition (C5)
+ils_status ils_slab_plan_create(ils_plan** out, int32_t height, int32_t width, const ils_params* params,
+                                int32_t dtype, int32_t device, int32_t nranks, int32_t rank) {
+  if (!out) return fail(ILS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (nranks < 1 || nranks > kMaxSeg) return fail(ILS_EINVAL, "nranks must be in [1, %d], got %d", kMaxSeg, nranks);
+  if (rank < 0 || rank >= nranks) return fail(ILS_EINVAL, "rank %d outside [0, %d)", rank, nranks);
+  if (width % 2) return fail(ILS_EUNSUPPORTED, "slab plans need an even width, got %d", width);
+  if (height < nranks) return fail(ILS_EINVAL, "height %d < nranks %d", height, nranks);
+  const int Wc = width / 2 + 1;
+  if (Wc < 2 * nranks + 1) return fail(ILS_EINVAL, "width %d too small for %d ranks", width, nranks);
+  ils_plan* p = nullptr;
+  // a host-only plan of the global shape for the FFT plans and tables, then
+  // the launch geometry re-planned for this rank's rows and columns
+  ils_status st = ils_plan_create(&p, 1, height, width, params, dtype, -1);
+  if (st != ILS_OK) return st;
+  p->slab = true;
+  p->P = nranks;
+  p->rank = rank;
+  for (int q = 0; q <= nranks; ++q) {
+    p->row0[q] = (int)((long long)q * height / nranks);
+    // even column offsets (16-byte aligned segments), balanced to within 2
+    p->col0[q] = q == nranks ? Wc : (int)(((long long)q * Wc / nranks) & ~1LL);
+  }
+  for (int q = 0; q < nranks; ++q) p->pitch[q] = (p->col0[q + 1] - p->col0[q] + 1) & ~1;
+  p->Hl = p->row0[rank + 1] - p->row0[rank];
+  p->Wcl = p->col0[rank + 1] - p->col0[rank];
+  if (device >= 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) p->sms = sms;
+  }
+  const size_t elt = dtype == ILS_F32 ? sizeof(cx<float>) : sizeof(cx<double>);
+  const int maxe = dtype == ILS_F32 ? 16 : 8;
+  const int H = p->H, Wcg = p->Wc;
+  p->H = p->Hl;  // row geometry over the local rows
+  bool ok = choose_row(*p, maxe, elt);
+  p->H = H;
+  p->Wc = p->Wcl;  // column geometry over the local columns
+  ok = ok && choose_col(*p, maxe, elt);
+  p->Wc = Wcg;
+  if (!ok) {
+    ils_plan_destroy(p);
+    return fail(ILS_EUNSUPPORTED, "no slab launch configuration for %dx%d on %d ranks", height, width, nranks);
+  }
+  p->device = device;
+  if (device >= 0) {  // device tables (same content as the host-only plan's)
+    const int rs = dtype == ILS_F32 ? 4 : 8;
+    (void)rs;
+    ils_plan* full = nullptr;
+    st = ils_plan_create(&full, 1, height, width, params, dtype, device);
+    if (st != ILS_OK) {
+      ils_plan_destroy(p);
+      return st;
+    }
+    p->d_tables = full->d_tables;  // take ownership of the uploaded tables
+    p->off_rowtw = full->off_rowtw;
+    p->off_coltw = full->off_coltw;
+    p->off_wreal = full->off_wreal;
+    p->off_wx = full->off_wx;
+    p->off_wy = full->off_wy;
+    p->off_sink = full->off_sink;
+    full->d_tables = nullptr;
+    ils_plan_destroy(full);
+  }
+  *out = p;
+  return ILS_OK;
+}
+
+ils_status ils_slab_get_layout(const ils_plan* p, int32_t* row0, int32_t* col0, int32_t* pitch, int64_t* counts) {
+  if (!p || !p->slab) return fail(ILS_EINVAL, "not a slab plan");
+  const int P = p->P, me = p->rank;
+  for (int q = 0; q <= P; ++q) {
+    if (row0) row0[q] = p->row0[q];
+    if (col0) col0[q] = p->col0[q];
+  }
+  for (int q = 0; q < P; ++q) {
+    if (pitch) pitch[q] = p->pitch[q];
+    if (counts) {  // complex elements: fwd send/recv, rev send/recv, per peer q
+      const int Hq = p->row0[q + 1] - p->row0[q];
+      counts[0 * kMaxSeg + q] = (int64_t)p->Hl * p->pitch[q];
+      counts[1 * kMaxSeg + q] = (int64_t)Hq * p->pitch[me];
+      counts[2 * kMaxSeg + q] = (int64_t)(Hq + 2) * p->pitch[me];
+      counts[3 * kMaxSeg + q] = (int64_t)(p->Hl + 2) * p->pitch[q];
+    }
+  }
+  return ILS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+template <typename T>
+ils_status slab_row_t(const ils_plan* p, int mode, const T* f_ext, const cx<T>* recv, cx<T>* send, T* u, int iter,
+                      cudaStream_t s, int32_t* status) {
+  RowArgs<T> a = row_args<T>(p);
+  a.H = p->Hl;
+  a.wrap = 0;
+  a.f = f_ext ? f_ext + p->W : nullptr;  // row -1 is the top halo row
+  a.f_ps = (long long)(p->Hl + 2) * p->W;
+  a.f_rp = p->W;
+  a.u = u;
+  a.u_ps = (long long)p->Hl * p->W;
+  a.u_rp = p->W;
+  a.status = status;
+  a.iter = iter;
+  a.Sin = recv;
+  a.Sout = send;
+  a.S_ps = 0;
+  long long in_off = 0, out_off = 0;
+  a.sin_seg.n = a.sout_seg.n = p->P;
+  for (int q = 0; q <= p->P; ++q) a.sin_seg.c0[q] = a.sout_seg.c0[q] = p->col0[q];
+  for (int q = 0; q < p->P; ++q) {
+    a.sin_seg.pitch[q] = a.sout_seg.pitch[q] = p->pitch[q];
+    a.sin_seg.off[q] = in_off + p->pitch[q];  // block row 1 = local row 0
+    a.sout_seg.off[q] = out_off;
+    in_off += (long long)(p->Hl + 2) * p->pitch[q];
+    out_off += (long long)p->Hl * p->pitch[q];
+  }
+  a.mode = mode;
+  const dim3 grid(p->row_grid, 1);
+  cudaError_t e;
+  if constexpr (std::is_same<T, float>::value) {
+    switch (p->row_spec) {
+#define ILS_CASE(ID, ...)                                                                                      \
+  case ID:                                                                                                     \
+    e = launch_row_impl<float, true, RowSpec<ID>::type, ILS_ROW_SPEC_WIDE(ID)>(a, grid, p->row_threads,        \
+                                                                             p->row_smem, s);                 \
+    if (e != cudaSuccess) return fail(ILS_ECUDA, "slab row pass: %s", cudaGetErrorString(e));                 \
+    return ILS_OK;
+      ILS_ROW_SPECS(ILS_CASE)
+#undef ILS_CASE
+      default:
+        break;
+    }
+  }
+  e = p->W > kNarrowMaxW ? launch_row_impl<T, true, FftRt, true>(a, grid, p->row_threads, p->row_smem, s)
+                         : launch_row_impl<T, true, FftRt>(a, grid, p->row_threads, p->row_smem, s);
+  if (e != cudaSuccess) return fail(ILS_ECUDA, "slab row pass: %s", cudaGetErrorString(e));
+  return ILS_OK;
+}
+
+template <typename T>
+ils_status slab_col_t(const ils_plan* p, cx<T>* recv, cx<T>* send, cudaStream_t s) {
+  ColArgs<T> c = col_args<T>(p, recv, COL_SOLVE);
+  const int me = p->rank;
+  c.Wc = p->Wcl;
+  c.S_rp = p->pitch[me];
+  c.S_ps = 0;
+  c.wx += p->col0[me];
+  c.P = p->P;
+  long long off = 0;
+  for (int q = 0; q <= p->P; ++q) c.r0[q] = p->row0[q];
+  for (int q = 0; q < p->P; ++q) {
+    c.dst_off[q] = off;
+    off += (long long)(p->row0[q + 1] - p->row0[q] + 2) * p->pitch[me];
+  }
+  c.dst = send;
+  const dim3 grid(p->col_grid, 1);
+  cudaError_t e;
+  if constexpr (std::is_same<T, float>::value) {
+    switch (p->col_spec) {
+#define ILS_CASE(ID, ...)                                                                    \
+  case ID:                                                                                   \
+    e = launch_col_impl<float, ColSpec<ID>::type>(c, grid, p->col_threads, p->col_smem, s);  \
+    if (e != cudaSuccess) return fail(ILS_ECUDA, "slab col pass: %s", cudaGetErrorString(e)); \
+    return ILS_OK;
+      ILS_COL_SPECS(ILS_CASE)
+#undef ILS_CASE
+      default:
+        break;
+    }
+  }
+  e = launch_col_impl<T, FftRt>(c, grid, p->col_threads, p->col_smem, s);
+  if (e != cudaSuccess) return fail(ILS_ECUDA, "slab col pass: %s", cudaGetErrorString(e));
+  return ILS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ils_status ils_slab_row_pass(const ils_plan* p, int32_t mode, const void* f_ext, const void* recv, void* send,
+                             void* u, int32_t iter, void* stream, int32_t* status) {
+  if (!p || !p->slab) return fail(ILS_EINVAL, "not a slab plan");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (mode != MODE_F0 && mode != MODE_IT && mode != MODE_FIN) return fail(ILS_EINVAL, "mode must be 0, 1 or 3");
+  if (!status || (mode != MODE_FIN && !send) || (mode != MODE_F0 && !recv) || (mode == MODE_FIN && !u) || !f_ext)
+    return fail(ILS_EINVAL, "NULL argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->dtype == ILS_F32)
+    return slab_row_t<float>(p, mode, static_cast<const float*>(f_ext), static_cast<const cx<float>*>(recv),
+                             static_cast<cx<float>*>(send), static_cast<float*>(u), iter, s, status);
+  return slab_row_t<double>(p, mode, static_cast<const double*>(f_ext), static_cast<const cx<double>*>(recv),
+                            static_cast<cx<double>*>(send), static_cast<double*>(u), iter, s, status);
+}
+
+ils_status ils_slab_col_pass(const ils_plan* p, void* recv, void* send, void* stream) {
+  if (!p || !p->slab) return fail(ILS_EINVAL, "not a slab plan");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (!recv || !send) return fail(ILS_EINVAL, "NULL argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->dtype == ILS_F32)
+    return slab_col_t<float>(p, static_cast<cx<float>*>(recv), static_cast<cx<float>*>(send), s);
+  return slab_col_t<double>(p, static_cast<cx<double>*>(recv), static_cast<cx<double>*>(send), s);
 }
 
 }  // extern "C"

@@ -311,11 +311,13 @@ __device__ __forceinline__ std::conditional_t<FIRST, Pre, NoPre> pick_pre(const 
 struct FftRt {
   static constexpr int n = 0;
   static constexpr int G = 0;
+  static constexpr int ME = 16;
 };
-template <int SWZ, int GG, int N, int... Rs>
+template <int SWZ, int GG, int ME_, int N, int... Rs>
 struct FftCt {
   static constexpr int n = N;
   static constexpr int G = GG;
+  static constexpr int ME = ME_;  // register budget: complex elements per thread per pass
   static constexpr int swz = SWZ;
   static constexpr int npass = sizeof...(Rs);
   static_assert((Rs * ... * 1) == N, "radix product must equal N");
@@ -331,10 +333,10 @@ struct RadixList {
   }
 };
 
-template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, class Pre, int... Is>
+template <typename T, int DIR, int SWZ, int GG, int MEX, int N, int... Rs, class Grp, class Pre, int... Is>
 __device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
                                                  const Pre& pre, std::integer_sequence<int, Is...>) {
-  constexpr int ME = MaxElems<T>::value;
+  constexpr int ME = MEX;
   using RL = RadixList<Rs...>;
   constexpr int NP = sizeof...(Rs);
   using LaySw = LayoutCt<T, SWZ>;
@@ -345,10 +347,10 @@ __device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const Ff
    ...);
 }
 
-template <typename T, int DIR, int SWZ, int GG, int N, int... Rs, class Grp, class Pre>
+template <typename T, int DIR, int SWZ, int GG, int MEX, int N, int... Rs, class Grp, class Pre>
 __device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Pre& pre,
-                                            FftCt<SWZ, GG, N, Rs...>) {
-  fft_line_ct_impl<T, DIR, SWZ, GG, N, Rs...>(x, P, g, pre, std::make_integer_sequence<int, sizeof...(Rs)>{});
+                                            FftCt<SWZ, GG, MEX, N, Rs...>) {
+  fft_line_ct_impl<T, DIR, SWZ, GG, MEX, N, Rs...>(x, P, g, pre, std::make_integer_sequence<int, sizeof...(Rs)>{});
 }
 
 // Full transform of one identity-laid line (DIR = -1 forward, +1 inverse,

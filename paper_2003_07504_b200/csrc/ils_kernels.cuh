@@ -51,9 +51,25 @@ struct PenaltyDev {
   T eps0, E, coef;
 };
 
+constexpr int kMaxSeg = 8;  // ranks of a slab-decomposed (distributed) transform
+
+// Spectrum rows split into column segments: the row-pass side of the
+// distributed FFT transpose.  Segment q holds columns
+// [c0[q], c0[q+1]) of every row at base + off[q] + row * pitch[q], i.e. the
+// all-to-all blocks [q][rows][cols_q], so the row pass reads what the
+// all-to-all delivered and writes what it sends, with no pack/unpack pass.
+// n = 0: plain rows (base + row * S_rp).
+struct SegRows {
+  int n;
+  int c0[kMaxSeg + 1];
+  long long off[kMaxSeg];
+  int pitch[kMaxSeg];  // even (16-byte rows for bulk copies)
+};
+
 template <typename T>
 struct RowArgs {
   int mode;  // RowMode
+  int wrap;  // 1: rows periodic in [0, H); 0: slab rows, halo rows -1 and H present
   int B, H, W, N, Wc, band, LP;
   const T* f;
   long long f_ps;
@@ -64,6 +80,7 @@ struct RowArgs {
   cx<T>* Sout;
   long long S_ps;
   int S_rp;
+  SegRows sin_seg, sout_seg;
   T* u;
   long long u_ps;
   int u_rp;
@@ -81,6 +98,13 @@ struct ColArgs {
   cx<T>* S;
   long long S_ps;
   int S_rp;
+  // distributed: scatter the result into per-destination blocks
+  // [rows of p plus its two halo rows][ncols] (the reverse all-to-all's send
+  // buffer) instead of writing it back in place.  P = 0: in place.
+  int P;
+  int r0[kMaxSeg + 1];
+  long long dst_off[kMaxSeg];
+  cx<T>* dst;
   const T* wx;  // 2 - 2 cos(2 pi kx / W), kx < Wc
   const T* wy;  // 2 - 2 cos(2 pi ky / H)
   T cl2;        // c * lam / 2
@@ -396,25 +420,42 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
         for (int i = 0; i < nl; ++i) mbar_init(&bars[i], 1);
         mbar_fence_init();
         for (int i = 0; i < nl; ++i) {
-          const int y = wrapi(y0 + i, H);
-          const void* src = MODE == MODE_F0 ? (const void*)(fpl + (size_t)y * A.f_rp)
-                                            : (const void*)(A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp);
-          const unsigned bytes = MODE == MODE_F0 ? (unsigned)(W * sizeof(T)) : spec_bytes;
-          mbar_expect_tx(&bars[i], bytes);
-          bulk_g2s(L.line(i), src, bytes, &bars[i]);
+          const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
+          if (MODE == MODE_F0) {
+            const unsigned bytes = (unsigned)(W * sizeof(T));
+            mbar_expect_tx(&bars[i], bytes);
+            bulk_g2s(L.line(i), fpl + (size_t)y * A.f_rp, bytes, &bars[i]);
+          } else if (A.sin_seg.n == 0) {
+            mbar_expect_tx(&bars[i], spec_bytes);
+            bulk_g2s(L.line(i), A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp, spec_bytes, &bars[i]);
+          } else {
+            const SegRows& sg = A.sin_seg;
+            unsigned total = 0;
+            for (int q = 0; q < sg.n; ++q) total += (unsigned)(((sg.c0[q + 1] - sg.c0[q] + 1) & ~1) * sizeof(cx<T>));
+            mbar_expect_tx(&bars[i], total);
+            for (int q = 0; q < sg.n; ++q)
+              bulk_g2s(L.line(i) + sg.c0[q], A.Sin + (size_t)b * A.S_ps + sg.off[q] + (long long)y * sg.pitch[q],
+                       (unsigned)(((sg.c0[q + 1] - sg.c0[q] + 1) & ~1) * sizeof(cx<T>)), &bars[i]);
+          }
         }
       }
       __syncthreads();
     } else if (MODE != MODE_F0 || PACKED) {
       for (int i = g.id; i < nl; i += ngroups) {
-        const int y = wrapi(y0 + i, H);
+        const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
         cx<T>* z = L.line(i);
         if (MODE == MODE_F0) {
           const cx<T>* src = reinterpret_cast<const cx<T>*>(fpl + (size_t)y * A.f_rp);
           for (int q = g.rank; q < W / 2; q += g.size()) cp_async<sizeof(cx<T>)>(z + q, src + q);
-        } else {
+        } else if (A.sin_seg.n == 0) {
           const cx<T>* src = A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp;
           for (int k = g.rank; k < A.Wc; k += g.size()) cp_async<sizeof(cx<T>)>(z + k, src + k);
+        } else {
+          const SegRows& sg = A.sin_seg;
+          for (int q = 0; q < sg.n; ++q) {
+            const cx<T>* src = A.Sin + (size_t)b * A.S_ps + sg.off[q] + (long long)y * sg.pitch[q] - sg.c0[q];
+            for (int k = sg.c0[q] + g.rank; k < sg.c0[q + 1]; k += g.size()) cp_async<sizeof(cx<T>)>(z + k, src + k);
+          }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
@@ -422,7 +463,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     bool bad = false;
     int li = 0;
     for (int i = g.id; i < nl; i += ngroups, ++li) {
-      const int y = wrapi(y0 + i, H);
+      const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
       cx<T>* z = L.line(i);
       if constexpr (BULK) {
         mbar_wait(&bars[i], 0);
@@ -612,11 +653,26 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
     fft_line<T, -1, FS>(z, A.fft, g);
     if (PACKED) r2c_post<T>(z, A.N, A.wreal, g);
     else g.sync();
-    cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
-    if constexpr (BULK) {
-      if (g.rank == 0) bulk_s2g(dst, z, spec_bytes);
+    if (A.sout_seg.n == 0) {
+      cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
+      if constexpr (BULK) {
+        if (g.rank == 0) bulk_s2g(dst, z, spec_bytes);
+      } else {
+        for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[k];
+      }
     } else {
-      for (int k = g.rank; k < A.Wc; k += g.size()) dst[k] = z[k];
+      // fused pack: each column segment goes straight into its destination's
+      // all-to-all block
+      const SegRows& sg = A.sout_seg;
+      for (int q = 0; q < sg.n; ++q) {
+        cx<T>* dst = A.Sout + (size_t)b * A.S_ps + sg.off[q] + (long long)(r0 + i) * sg.pitch[q];
+        if constexpr (BULK) {
+          if (g.rank == 0)
+            bulk_s2g(dst, z + sg.c0[q], (unsigned)(((sg.c0[q + 1] - sg.c0[q] + 1) & ~1) * sizeof(cx<T>)));
+        } else {
+          for (int k = sg.c0[q] + g.rank; k < sg.c0[q + 1]; k += g.size()) dst[k - sg.c0[q]] = z[k];
+        }
+      }
     }
   }
   if constexpr (BULK) bulk_wait_reads();
@@ -640,8 +696,12 @@ struct UniformScale {
 // A strip of C columns is loaded transposed into C lines (line pitch CS
 // chosen so the transposing copies are bank-conflict-free); a group owns one
 // column at a time: forward FFT, * 1/(H W denom), inverse FFT.
+// plans holding more than 16 elements per thread get the 2-CTA register budget
+template <class FS>
+constexpr int kColBlocksOf = FS::ME > 16 ? 2 : kColMinBlocks;
+
 template <typename T, class FS>
-__global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_col(const ColArgs<T> A) {
+__global__ void __launch_bounds__(kColThreads, kColBlocksOf<FS>) k_col(const ColArgs<T> A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
   T* swy = reinterpret_cast<T*>(tile + A.C * A.CS);  // wy[0..H) staged once per CTA
@@ -679,8 +739,32 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_col(const ColArg
     }
   }
   __syncthreads();
-  if (copier)
-    for (int y = y0; y < H; y += ystep) Spl[(size_t)y * A.S_rp + cc] = tile[cc * A.CS + y];
+  if (A.P == 0) {
+    if (copier)
+      for (int y = y0; y < H; y += ystep) Spl[(size_t)y * A.S_rp + cc] = tile[cc * A.CS + y];
+    return;
+  }
+  // distributed: row y goes to its owner p (block row y - r0[p] + 1) and, when
+  // it is p's first / last row, also to p-1 / p+1 as their bottom / top halo
+  // (periodic across ranks): the reverse transpose plus the halo exchange in
+  // one scatter (fused pack)
+  if (copier) {
+    cx<T>* dpl = A.dst + (size_t)b * A.S_ps + c0 + cc;
+    int p = 0;
+    for (int y = y0; y < H; y += ystep) {
+      while (y >= A.r0[p + 1]) ++p;
+      const cx<T> v = tile[cc * A.CS + y];
+      dpl[A.dst_off[p] + (long long)(y - A.r0[p] + 1) * A.S_rp] = v;
+      if (y == A.r0[p]) {
+        const int q = p == 0 ? A.P - 1 : p - 1;
+        dpl[A.dst_off[q] + (long long)(A.r0[q + 1] - A.r0[q] + 1) * A.S_rp] = v;
+      }
+      if (y == A.r0[p + 1] - 1) {
+        const int q = p == A.P - 1 ? 0 : p + 1;
+        dpl[A.dst_off[q]] = v;
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------ small kernels
@@ -721,11 +805,11 @@ __global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long n
 // Compile-time FFT plans for the hot sizes (fp32).  Everything else runs the
 // runtime-planned path (FftRt).  The host planner (ils_api.cu) uses exactly
 // these radix lists when n matches, so twiddle tables and kernels agree.
-// X(id, swizzle, group threads, n, radices...)
-#define ILS_ROW_SPECS(X) X(0, 1, 32, 256, 16, 16) X(1, 2, 32, 960, 32, 30) X(2, 1, 128, 1920, 16, 15, 8) X(3, 1, 256, 3840, 16, 16, 15) X(4, 1, 32, 512, 16, 8, 4)
+// X(id, swizzle, group threads, elements per thread, n, radices...)
+#define ILS_ROW_SPECS(X) X(0, 1, 32, 16, 256, 16, 16) X(1, 2, 32, 32, 960, 32, 30) X(2, 1, 128, 16, 1920, 16, 15, 8) X(3, 1, 256, 16, 3840, 16, 16, 15) X(4, 1, 32, 16, 512, 16, 8, 4)
 // row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
 #define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)
-#define ILS_COL_SPECS(X) X(0, 1, 32, 512, 16, 8, 4) X(1, 0, 128, 1080, 15, 9, 8) X(2, 1, 256, 2160, 16, 15, 9) X(3, 1, 32, 256, 16, 16) X(4, 1, 128, 720, 16, 9, 5)
+#define ILS_COL_SPECS(X) X(0, 1, 32, 16, 512, 16, 8, 4) X(1, 0, 128, 16, 1080, 15, 9, 8) X(2, 1, 256, 16, 2160, 16, 15, 9) X(3, 1, 32, 16, 256, 16, 16) X(4, 1, 128, 16, 720, 16, 9, 5) X(5, 1, 256, 24, 4320, 24, 18, 10)
 
 template <int ID>
 struct RowSpec;

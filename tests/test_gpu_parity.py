@@ -233,3 +233,32 @@ def test_torch_zero_copy_path_matches_numpy_path():
     u_np = ils.smooth_plane(f, params)
     u_t = ils.smooth_plane(torch.from_numpy(f).to("cuda", torch.float32), params)
     assert np.array_equal(u_np, u_t.double().cpu().numpy())
+
+
+# ------------------------------------------------------------ C5 slab decomposition (emulated ranks)
+@pytest.mark.parametrize("H,W,P", [(1080, 1920, 2), (1080, 1920, 3), (256, 320, 4), (90, 128, 8)])
+def test_slab_decomposition_bitwise_equals_single_gpu(H, W, P):
+    from paper_2003_07504_b200.dist import EmulatedSlab
+
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0, iters=4)
+    f = torch.from_numpy(np.random.default_rng(11).random((H, W))).to("cuda", torch.float32)
+    one = ils.smooth_batch(f[None], params)[0]
+    em = EmulatedSlab(H, W, params, P)
+    u = em.smooth(f)
+    assert torch.equal(u, one)  # bitwise: every line is transformed by the same code wherever it lives
+
+
+def test_c5_8k_texture_slab_and_wide_rows():
+    # C5: 7680x4320, Welsch g=10/255, lam=30, N=10, c=2 (texture parameters, no pre-blur)
+    from paper_2003_07504_b200.dist import EmulatedSlab
+
+    params = ils.SmoothParams(ils.Welsch(10 / 255), 30.0, iters=10, c=2.0)
+    f = torch.from_numpy(np.random.default_rng(20240607).random((4320, 7680))).to("cuda", torch.float32)
+    one = ils.smooth_batch(f[None], params)[0]
+    u8 = EmulatedSlab(4320, 7680, params, 8).smooth(f)
+    assert torch.equal(u8, one)
+    # parity of the wide-row path vs the oracle on a band-limited crop of the same width
+    fc = np.random.default_rng(3).random((120, 7680))
+    uc = ils.smooth_plane(fc, params)
+    ref = O.smooth_plane(fc, O.Welsch(10 / 255), 30.0, 10, c=2.0)
+    assert np.max(np.abs(uc - ref)) <= 1e-4
