@@ -277,6 +277,13 @@ size_t esz() {
 }
 
 template <size_t K>
+int spec_me(const SpecHost (&tab)[K], int id) {
+  for (const SpecHost& s : tab)
+    if (s.id == id) return s.me;
+  return 16;
+}
+
+template <size_t K>
 const SpecHost* find_spec(const SpecHost (&tab)[K], int n) {
   if (env_int("ILS_NO_SPECS", 0)) return nullptr;
   for (const SpecHost& s : tab)
@@ -304,11 +311,14 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
     if (force && band != std::min(force, p.H)) continue;
     const size_t smem = (size_t)(band + 2) * LP * elt;
     if (smem > 227 * 1024) break;
-    const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+    // resident CTAs/SM: register budget (kRowBlocksOf: 3 for <= 16 elements per
+    // thread compile-time plans) and 228 KB of shared memory
+    const int reg_cap = (p.row_spec >= 0 && spec_me(kRowSpecs, p.row_spec) <= 16) ? 3 : 2;
+    const int per_sm = (int)std::min<size_t>(reg_cap, (228 * 1024) / (smem + 1024));
     const long ctas = (long)p.B * ((p.H + band - 1) / band);
     // issue-bound: time ~ the busiest SM's work (b+2 c2r, b r2c, b stencil rows)
     const double per_sm_ctas = (double)((ctas + p.sms - 1) / p.sms);
-    const double cost = per_sm_ctas * (2.5 * band + 2.0) * (per_sm == 1 ? 1.5 : 1.0);
+    const double cost = per_sm_ctas * (2.5 * band + 2.0) * (per_sm == 1 ? 1.5 : per_sm == 2 ? 1.0 : 0.9);
     if (cost < best * (1 - 1e-9)) {
       best = cost;
       p.band = band;

@@ -344,8 +344,12 @@ constexpr bool kBulkRows = sizeof(T) == 4 && FS::n > 0 && (2 * FS::n) % 8 == 0;
 // SMODE >= 0: kernel specialised for that mode without trace (the hot
 // kernels; dead phases compiled out keeps the code inside the I-cache);
 // SMODE = -1: any mode from A.mode, optional energy trace.
+// register budget: 3 CTAs / SM for plans with <= 16 elements per thread, else 2
+template <class FS>
+constexpr int kRowBlocksOf = (FS::n > 0 && FS::ME <= 16) ? 3 : 2;
+
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
-__global__ void __launch_bounds__(kRowThreads, 2) k_row(const RowArgs<T> A) {
+__global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ unsigned long long bars[kMaxBandLines];
