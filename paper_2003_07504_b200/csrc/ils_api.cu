@@ -302,14 +302,16 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   const int line = p.packed ? p.N + 1 : p.N;
   // a swizzled layout permutes inside whole 128-byte blocks: round up to them
   const int E = elt == 8 ? 16 : 8;
-  const int LP = p.rowf.swz ? (line + E - 1) / E * E : (line + 1) & ~1;
+  // interior passes swizzle elements < n inside whole 128-byte blocks
+  const int LP = std::max(p.rowf.swz ? (p.N + E - 1) / E * E : 0, (line + 1) & ~1);
+  const size_t wreal_bytes = p.packed ? (size_t)(p.N / 2 + 1) * elt : 0;  // staged twiddles
   // Band size: minimise (waves x per-CTA work).  A CTA of band b transforms
   // b+2 lines c2r and b lines r2c; 2 CTAs fit an SM while smem <= ~113 KB.
   const int force = env_int("ILS_ROW_BAND", 0);
   double best = 1e300;
   for (int band = 1; band <= std::min(p.H, kMaxBandLines - 2); ++band) {
     if (force && band != std::min(force, p.H)) continue;
-    const size_t smem = (size_t)(band + 2) * LP * elt;
+    const size_t smem = (size_t)(band + 2) * LP * elt + wreal_bytes;
     if (smem > 227 * 1024) break;
     // resident CTAs/SM: register budget (kRowBlocksOf: 3 for <= 16 elements per
     // thread compile-time plans) and 228 KB of shared memory

@@ -151,7 +151,7 @@ struct NoPre {
 template <typename T, int R, int KM, int DIR, class Grp, class LayI, class LayO, class Pre = NoPre>
 __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, const cx<T>* __restrict__ tw,
                                          const Grp& g, const LayI& lay_in, const LayO& lay_out,
-                                         const Pre& pre = Pre{}) {
+                                         const Pre& pre = Pre{}, const cx<T>* wcache = nullptr) {
   // Idle slots (j >= nb) recompute the last butterfly instead of skipping it:
   // conditionally-defined register arrays become loop-carried live ranges in
   // the caller's line loop and triple the register footprint.
@@ -167,7 +167,9 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
       // radices w^(8a+b) = (w^8)^a w^b (two short chains instead of one long).
       // Loading all R-1 powers measured slower (load latency on the critical
       // path of every pass).
-      cx<T> w1 = ldtw(tw + (j % Ns));
+      // base twiddle: from the per-thread cache (compile-time plans: it only
+      // depends on the thread's rank, so it is loaded once per kernel) or the table
+      cx<T> w1 = wcache ? wcache[k] : ldtw(tw + (j % Ns));
       if (DIR > 0) w1.y = -w1.y;
       if constexpr (R <= 16) {
         cx<T> w = w1;
@@ -311,7 +313,8 @@ __device__ __forceinline__ std::conditional_t<FIRST, Pre, NoPre> pick_pre(const 
 struct FftRt {
   static constexpr int n = 0;
   static constexpr int G = 0;
-  static constexpr int ME = 16;
+  static constexpr int ME = 1;  // no twiddle cache for runtime plans
+  static constexpr int npass = 0;
 };
 template <int SWZ, int GG, int ME_, int N, int... Rs>
 struct FftCt {
@@ -333,9 +336,43 @@ struct RadixList {
   }
 };
 
+// Per-thread base twiddles of a compile-time plan: pass p, slot k holds
+// w_{Ns R}^(j mod Ns) for j = min(rank + k G, n/R - 1) -- the same for every
+// line the thread transforms, so a kernel loads them once (fill_twcache).
+template <typename T, class S>
+struct TwCache {
+  static constexpr int NP = S::npass > 0 ? S::npass : 1;
+  static constexpr int KX = S::ME;  // >= KM of every pass
+  cx<T> w[NP][KX];
+};
+
+template <typename T, int SWZ, int GG, int MEX, int N, int... Rs, class Grp, int... Is>
+__device__ __forceinline__ void fill_twcache_impl(TwCache<T, FftCt<SWZ, GG, MEX, N, Rs...>>& c, const FftDev<T>& P,
+                                                  const Grp& g, std::integer_sequence<int, Is...>) {
+  using RL = RadixList<Rs...>;
+  auto one = [&](auto I) {
+    constexpr int p = ILS_CV(I);
+    constexpr int R = RL::r[p], nb = N / R, Ns = RL::ns(p), KM = KmOf<R, MEX>::value;
+    if constexpr (Ns > 1) {
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const int j = min(g.rank + k * g.size(), nb - 1);
+        c.w[p][k] = ldg_cx(P.tw + P.tw_off[p] + (j % Ns));
+      }
+    }
+  };
+  (one(std::integral_constant<int, Is>{}), ...);
+}
+
+template <typename T, class S, class Grp>
+__device__ __forceinline__ void fill_twcache(TwCache<T, S>& c, const FftDev<T>& P, const Grp& g) {
+  if constexpr (S::n > 0) fill_twcache_impl(c, P, g, std::make_integer_sequence<int, S::npass>{});
+}
+
 template <typename T, int DIR, int SWZ, int GG, int MEX, int N, int... Rs, class Grp, class Pre, int... Is>
 __device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
-                                                 const Pre& pre, std::integer_sequence<int, Is...>) {
+                                                 const Pre& pre, const TwCache<T, FftCt<SWZ, GG, MEX, N, Rs...>>* tc,
+                                                 std::integer_sequence<int, Is...>) {
   constexpr int ME = MEX;
   using RL = RadixList<Rs...>;
   constexpr int NP = sizeof...(Rs);
@@ -343,21 +380,23 @@ __device__ __forceinline__ void fft_line_ct_impl(cx<T>* __restrict__ x, const Ff
   (fft_pass<T, RL::r[Is], KmOf<RL::r[Is], ME>::value, DIR>(
        x, N / RL::r[Is], RL::ns(Is), P.tw + P.tw_off[Is], g,
        std::conditional_t<Is == 0, LayoutId, LaySw>{}, std::conditional_t<Is == NP - 1, LayoutId, LaySw>{},
-       std::conditional_t<Is == 0, Pre, NoPre>(pick_pre<Is == 0>(pre))),
+       std::conditional_t<Is == 0, Pre, NoPre>(pick_pre<Is == 0>(pre)), tc ? tc->w[Is] : nullptr),
    ...);
 }
 
 template <typename T, int DIR, int SWZ, int GG, int MEX, int N, int... Rs, class Grp, class Pre>
 __device__ __forceinline__ void fft_line_ct(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g, const Pre& pre,
+                                            const TwCache<T, FftCt<SWZ, GG, MEX, N, Rs...>>* tc,
                                             FftCt<SWZ, GG, MEX, N, Rs...>) {
-  fft_line_ct_impl<T, DIR, SWZ, GG, MEX, N, Rs...>(x, P, g, pre, std::make_integer_sequence<int, sizeof...(Rs)>{});
+  fft_line_ct_impl<T, DIR, SWZ, GG, MEX, N, Rs...>(x, P, g, pre, tc,
+                                                   std::make_integer_sequence<int, sizeof...(Rs)>{});
 }
 
 // Full transform of one identity-laid line (DIR = -1 forward, +1 inverse,
 // unnormalised).  Every thread of the group must call it.
 template <typename T, int DIR, class S, class Grp, class Pre = NoPre>
 __device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>& P, const Grp& g,
-                                         const Pre& pre = Pre{}) {
+                                         const Pre& pre = Pre{}, const TwCache<T, S>* tc = nullptr) {
   if constexpr (S::n == 0) {
     if constexpr (!std::is_same<Pre, NoPre>::value) {  // runtime plans: apply the map as its own sweep
       for (int e = g.rank; e < P.n; e += g.size()) x[e] = pre(e, x[e]);
@@ -365,7 +404,7 @@ __device__ __forceinline__ void fft_line(cx<T>* __restrict__ x, const FftDev<T>&
     }
     fft_line_rt<T, DIR>(x, P, g);
   } else {
-    fft_line_ct<T, DIR>(x, P, g, pre, S{});
+    fft_line_ct<T, DIR>(x, P, g, pre, tc, S{});
   }
 }
 

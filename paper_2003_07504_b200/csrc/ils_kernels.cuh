@@ -288,7 +288,7 @@ __device__ __forceinline__ void bulk_wait_reads() {
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
 // O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
 template <typename T, class Grp>
-__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g) {
+__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* wreal, const Grp& g) {
   for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
       const cx<T> z0 = z[0];
@@ -299,7 +299,7 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restric
       const cx<T> E{T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y)};
       const cx<T> d{T(0.5) * (zk.x - zm.x), T(0.5) * (zk.y + zm.y)};  // (zk - conj zm)/2
       const cx<T> O{d.y, -d.x};                                          // -i * d
-      const cx<T> wO = cmul(ldg_cx(wreal + k), O);
+      const cx<T> wO = cmul(wreal[k], O);
       z[k] = E + wO;
       if (N - k != k) z[N - k] = conj(E - wO);
     }
@@ -311,7 +311,7 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* __restric
 // E = X_k + conj X_{N-k}, O = (X_k - conj X_{N-k}) conj(w^k).  An inverse
 // N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
 template <typename T, class Grp>
-__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict__ wreal, const Grp& g) {
+__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* wreal, const Grp& g) {
   for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
       const T a = z[0].x, c = z[N].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
@@ -320,7 +320,7 @@ __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* __restrict
       const cx<T> xk = z[k], xm = z[N - k];
       const cx<T> E{xk.x + xm.x, xk.y - xm.y};
       const cx<T> D{xk.x - xm.x, xk.y + xm.y};
-      const cx<T> O = cmulc(D, ldg_cx(wreal + k));
+      const cx<T> O = cmulc(D, wreal[k]);
       z[k] = cx<T>{E.x - O.y, E.y + O.x};
       if (N - k != k) z[N - k] = cx<T>{E.x + O.y, -E.y + O.x};
     }
@@ -372,6 +372,14 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   const Lines<T, PACKED> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP};
   const PenaltyDev<T>& P = A.pen;
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
+  // real-packing twiddles staged in shared memory after the band's lines
+  cx<T>* swreal = reinterpret_cast<cx<T>*>(smem_raw) + (size_t)(A.band + 2) * A.LP;
+  if (PACKED) {
+    for (int k = tid; k <= A.N / 2; k += nthr) swreal[k] = A.wreal[k];
+    __syncthreads();
+  }
+  TwCache<T, FS> twc;
+  fill_twcache(twc, A.fft, g);
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
 
   if (MODE == MODE_IT && tid < nb && (W * sizeof(T)) % 16 == 0 && (A.f_rp * sizeof(T)) % 16 == 0) {
@@ -480,14 +488,14 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
         if (PACKED) {
-          c2r_pre<T>(z, A.N, A.wreal, g);
+          c2r_pre<T>(z, A.N, swreal, g);
         } else {
           // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
           for (int k = A.Wc + g.rank; k < W; k += g.size()) z[k] = conj(z[W - k]);
           if (g.rank == 0) z[0].y = T(0);
           g.sync();
         }
-        fft_line<T, +1, FS>(z, A.fft, g);
+        fft_line<T, +1, FS>(z, A.fft, g, NoPre{}, &twc);
       }
     }
     __syncthreads();
@@ -654,8 +662,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   // ---------------- phase C: r2c of rhs rows -> S_out (group per line)
   for (int i = g.id; i < nb; i += ngroups) {
     cx<T>* z = L.line(i);
-    fft_line<T, -1, FS>(z, A.fft, g);
-    if (PACKED) r2c_post<T>(z, A.N, A.wreal, g);
+    fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
+    if (PACKED) r2c_post<T>(z, A.N, swreal, g);
     else g.sync();
     if (A.sout_seg.n == 0) {
       cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
@@ -719,6 +727,8 @@ __global__ void __launch_bounds__(kColThreads, kColBlocksOf<FS>) k_col(const Col
   const int nc = min(A.C, A.Wc - c0);
   const int H = A.H;
   cx<T>* Spl = A.S + (size_t)b * A.S_ps + c0;
+  TwCache<T, FS> twc;
+  fill_twcache(twc, A.fft, g);
   // transposing copies: thread -> (column cc, first row y0), rows step ystep
   const int ystep = nthr / nc, cc = tid % nc, y0 = tid / nc;
   const bool copier = tid < ystep * nc;
@@ -730,16 +740,16 @@ __global__ void __launch_bounds__(kColThreads, kColBlocksOf<FS>) k_col(const Col
   __syncthreads();
   for (int c = g.id; c < nc; c += ngroups) {
     cx<T>* z = tile + c * A.CS;
-    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g);
+    if (A.mode != COL_INV) fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
     if (A.mode == COL_SOLVE) {
       // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses,
       // applied as the inverse transform's first pass loads each element
       const T base = T(1) + A.cl2 * __ldg(A.wx + c0 + c);
       const DenomScale<T> pre{swy, base, A.cl2, A.inv_hw};
-      fft_line<T, +1, FS>(z, A.fft, g, pre);
+      fft_line<T, +1, FS>(z, A.fft, g, pre, &twc);
     } else if (A.mode == COL_INV) {
       const UniformScale<T> pre{A.inv_hw};
-      fft_line<T, +1, FS>(z, A.fft, g, pre);
+      fft_line<T, +1, FS>(z, A.fft, g, pre, &twc);
     }
   }
   __syncthreads();
