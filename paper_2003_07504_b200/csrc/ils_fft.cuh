@@ -159,6 +159,14 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
 #pragma unroll
   for (int k = 0; k < KM; ++k) {
     const int j = min(g.rank + k * g.size(), nb - 1);
+    // warps whose lanes all fall past the last butterfly skip the work (a
+    // warp-uniform branch); the array stays defined so the allocator sees no
+    // loop-carried undefined values
+    if (((g.rank & ~31) + k * g.size()) >= nb) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[k][r] = cx<T>{T(0), T(0)};
+      continue;
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) v[k][r] = pre(j + r * nb, x[lay_in(j + r * nb)]);
     if (Ns > 1) {
