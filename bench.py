@@ -278,8 +278,40 @@ def main():
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    ms_row = time_pass(2)
-    ms_col = time_pass(1)
+    def time_in_sequence(frames=4):
+        """Per-kernel CUDA-event durations inside the real pass sequence (warm L2).
+
+        Replays the per-frame order F0, col, (IT, col) x (N-1), FIN through
+        ils_launch_pass with an event pair around every launch.
+        """
+        order = [0, 1] + [2, 1] * (ITERS - 1) + [3]
+        acc = {p: [] for p in (0, 1, 2, 3)}
+        with torch.cuda.stream(stream):
+            for rep in range(2):  # first pass warms plans and L2
+                # hold the stream while the launches are queued, so no host
+                # submission gap lands between an event pair
+                torch.cuda._sleep(200_000_000)
+                evs = []
+                for fr in range(frames):
+                    off = (fr % (F // G)) * G * CH * ps * 4
+                    for p in order:
+                        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a_.record(stream)
+                        _lib.check(L.ils_launch_pass(plan.ptr, p, C.c_void_p(f.data_ptr() + off),
+                                                     C.c_void_p(u.data_ptr() + off), ps, C.c_void_p(ws.data_ptr()),
+                                                     C.c_void_p(stream.cuda_stream), C.c_void_p(status.data_ptr())),
+                                   "ils_launch_pass")
+                        b_.record(stream)
+                        evs.append((p, a_, b_))
+                torch.cuda.synchronize()
+                if rep == 1:
+                    for p, a_, b_ in evs:
+                        acc[p].append(a_.elapsed_time(b_))
+        return {p: sum(v) / len(v) for p, v in acc.items()}
+
+    seq = time_in_sequence()
+    ms_row, ms_col = seq[2], seq[1]
+    ms_row_isolated, ms_col_isolated = time_pass(2), time_pass(1)
     wc = W // 2 + 1
     planes_g = G * CH
     row_bytes = planes_g * (2 * H * wc * 8 + H * W * 4)
@@ -344,9 +376,14 @@ def main():
                          "frac": round(row_gbs / peak, 4), "traffic": measured_traffic("k_row_it"),
                          "traffic_source": "profiles/traffic.json (ncu --set full, warm L2)", "peak_kind": peak_kind,
                          "kernel": "k_row fused row pass (iteration>=1)", "ms": round(ms_row, 4),
+                         "timing": "CUDA events around each launch inside the per-frame pass sequence (warm L2)",
+                         "ms_isolated_loop": round(ms_row_isolated, 4),
+                         "pass_ms_in_sequence": {"row_f0": round(seq[0], 4), "col": round(seq[1], 4),
+                                                 "row_it": round(seq[2], 4), "row_fin": round(seq[3], 4)},
                          "bytes_per_launch": row_bytes,
                          "col_pass": {"achieved": round(col_gbs, 1), "frac": round(col_gbs / peak, 4),
-                                      "ms": round(ms_col, 4), "bytes_per_launch": col_bytes},
+                                      "ms": round(ms_col, 4), "ms_isolated_loop": round(ms_col_isolated, 4),
+                                      "bytes_per_launch": col_bytes},
                          "whole_path": {"achieved": round(bpf * value / world / 1e9, 1),
                                         "frac": round(bpf * value / world / 1e9 / peak, 4),
                                         "bytes_per_frame": bpf}},

@@ -329,6 +329,12 @@ __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* wreal, con
 }
 
 // ------------------------------------------------------------ row pass
+template <typename T>
+struct AddPair {  // element e of a packed line += (f[2e], f[2e+1])
+  const cx<T>* f;
+  __device__ __forceinline__ cx<T> operator()(int e, cx<T> v) const { return v + ldg_cx(f + e); }
+};
+
 constexpr int kRowThreads = 256;
 constexpr int kColThreads = 256;
 constexpr int kColMinBlocks = 3;  // k_col register budget: 3 CTAs / SM
@@ -571,7 +577,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           for (int q = 0; q < QW; ++q) {
             const int x = gg * QW + q;
             myup[gi][q] = x < W ? aux(L.get(1, x) - L.get(0, x), P) : T(0);
-            fcur[gi][q] = (is_it && x < W) ? __ldg(fpl + (size_t)r0 * A.f_rp + x) : T(0);
+            fcur[gi][q] = (TR && is_it && x < W) ? __ldg(fpl + (size_t)r0 * A.f_rp + x) : T(0);
           }
         }
       }
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           if (gg < ng) {
             const int x0 = gg * QW;
             const bool full = PACKED && x0 + QW <= W;
-            if (is_it) {
+            if (TR && is_it) {
               const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp + x0;
 #pragma unroll
               for (int q = 0; q < QW; ++q) fnext[gi][q] = (full || x0 + q < W) ? __ldg(fr + q) : T(0);
@@ -613,8 +619,11 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
                 const T mxq = aux(gx, P);
                 const T myq = aux(gy, P);
                 const T a = (mxp - mxq) + (myup[gi][q] - myq);
+                // iteration >= 1: rhs holds lam/2 D^T mu only; f is added as the
+                // r2c's first pass loads each element (phase C), off the
+                // stencil's critical path
                 const T fv = is_it ? fcur[gi][q] : uc[q];
-                rhs[gi][q] = fma_rn(P.lam2, a, fv);
+                rhs[gi][q] = is_it ? mul_rn(P.lam2, a) : fma_rn(P.lam2, a, fv);
                 chk = fma_rn(uc[q], T(0), chk);
                 if constexpr (TR) {
                   const T d = uc[q] - fv;
@@ -642,7 +651,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
                 if (x0 + q < W) L.set(j, x0 + q, rhs[gi][q]);
             }
 #pragma unroll
-            for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
+            if (TR)
+              for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
           }
         }
       }
@@ -662,7 +672,16 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   // ---------------- phase C: r2c of rhs rows -> S_out (group per line)
   for (int i = g.id; i < nb; i += ngroups) {
     cx<T>* z = L.line(i);
-    fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
+    if (MODE == MODE_IT && PACKED) {
+      // rhs = f + lam/2 D^T mu: the f row is added as the first pass loads
+      // (independent coalesced loads, latency overlapped with the butterflies)
+      const AddPair<T> pre{reinterpret_cast<const cx<T>*>(fpl + (size_t)(r0 + i) * A.f_rp)};
+      fft_line<T, -1, FS>(z, A.fft, g, pre, &twc);
+    } else {
+      if (MODE == MODE_IT)  // unpacked (odd W): add f as its own sweep
+        for (int x = g.rank; x < W; x += g.size()) z[x].x += fpl[(size_t)(r0 + i) * A.f_rp + x];
+      fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
+    }
     if (PACKED) r2c_post<T>(z, A.N, swreal, g);
     else g.sync();
     if (A.sout_seg.n == 0) {
