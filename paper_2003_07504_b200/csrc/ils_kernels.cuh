@@ -266,6 +266,29 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "r"(phase)
       : "memory");
 }
+// L2 eviction policies for bulk copies: data that is dead after this use
+// (the spectrum a row pass consumes, the output u) is marked evict-first so it
+// does not push the frame's live working set (f, the next spectrum) out of L2
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* dst, const void* src, unsigned bytes, unsigned long long policy) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(policy)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -445,7 +468,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
             bulk_g2s(L.line(i), fpl + (size_t)y * A.f_rp, bytes, &bars[i]);
           } else if (A.sin_seg.n == 0) {
             mbar_expect_tx(&bars[i], spec_bytes);
-            bulk_g2s(L.line(i), A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp, spec_bytes, &bars[i]);
+            bulk_g2s_hint(L.line(i), A.Sin + (size_t)b * A.S_ps + (size_t)y * A.S_rp, spec_bytes, &bars[i],
+                          l2_evict_first());
           } else {
             const SegRows& sg = A.sin_seg;
             unsigned total = 0;
@@ -519,7 +543,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         }
         if constexpr (BULK) {
           __syncthreads();
-          if (tid < nb) bulk_s2g(upl + (size_t)(r0 + tid) * A.u_rp, L.line(tid + off), (unsigned)(W * sizeof(T)));
+          if (tid < nb)
+            bulk_s2g_hint(upl + (size_t)(r0 + tid) * A.u_rp, L.line(tid + off), (unsigned)(W * sizeof(T)),
+                          l2_evict_first());
         } else {
           const int np = W / 2;
           for (int j = 0; j < nb; ++j) {
