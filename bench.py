@@ -21,6 +21,9 @@ roofline  the dominant kernel (fused row pass, iterations >= 1) timed alone
           measured HBM copy bandwidth in MEASURED_PEAKS.json.
 cpu_baseline  the oracle port (numpy/scipy, the reference's own algorithm)
           on the host cores, one frame.
+cufft     the same loop written with torch.fft.rfft2/irfft2 (cuFFT) and
+          torch elementwise ops in fp32, one CUDA graph per step,
+          timed in the same run; its output is checked against ours.
 --impl reference  times that CPU path alone, as the driver's reference arm.
 """
 
@@ -118,6 +121,30 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def cufft_loop(f, lam, iters, p, eps, c):
+    """ILS with cuFFT + torch elementwise (comparison leg only, fp32, half spectra)."""
+    import math
+
+    import torch
+
+    h, w = f.shape[-2:]
+    wx = 2 - 2 * torch.cos(2 * math.pi * torch.arange(w // 2 + 1, device=f.device, dtype=torch.float64) / w)
+    wy = 2 - 2 * torch.cos(2 * math.pi * torch.arange(h, device=f.device, dtype=torch.float64) / h)
+    denom = (1 + c * lam / 2 * (wy[:, None] + wx[None, :])).float()
+    ff = torch.fft.rfft2(f)
+
+    def aux(x):
+        return c * x - p * x * torch.pow(x * x + eps, p / 2 - 1)
+
+    u = f
+    for _ in range(iters):
+        mx = aux(torch.roll(u, -1, -1) - u)
+        my = aux(torch.roll(u, -1, -2) - u)
+        a = torch.roll(mx, 1, -1) - mx + torch.roll(my, 1, -2) - my
+        u = torch.fft.irfft2((ff + lam / 2 * torch.fft.rfft2(a)) / denom, s=(h, w))
+    return u
+
+
 def cpu_port_frame_seconds(frames=1, seed=20240607, warm=True):
     """Oracle port (the reference algorithm, numpy + scipy.fft) on one 1080p RGB frame."""
     from oracle import ils_oracle as O
@@ -170,6 +197,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT + torch comparison leg")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -284,7 +312,11 @@ def main():
         Replays the per-frame order F0, col, (IT, col) x (N-1), FIN through
         ils_launch_pass with an event pair around every launch.
         """
-        order = [0, 1] + [2, 1] * (ITERS - 1) + [3]
+        order = [0, 1]
+        for n in range(1, ITERS):  # current spectrum alternates A/B (pass | 4 = B current)
+            cur = 0 if n % 2 else 4
+            order += [2 | cur, 1 | (cur ^ 4)]
+        order += [3 | (0 if ITERS % 2 else 4)]
         acc = {p: [] for p in (0, 1, 2, 3)}
         with torch.cuda.stream(stream):
             for rep in range(2):  # first pass warms plans and L2
@@ -306,10 +338,13 @@ def main():
                 torch.cuda.synchronize()
                 if rep == 1:
                     for p, a_, b_ in evs:
-                        acc[p].append(a_.elapsed_time(b_))
+                        acc[p & 3].append(a_.elapsed_time(b_))
         return {p: sum(v) / len(v) for p, v in acc.items()}
 
+    u_graph = u[:CH].clone()
     seq = time_in_sequence()
+    # the per-pass replay is the real dataflow: it reproduces the graph's output bit for bit
+    assert torch.equal(u[:CH], u_graph), "per-pass sequence differs from ils_smooth"
     ms_row, ms_col = seq[2], seq[1]
     ms_row_isolated, ms_col_isolated = time_pass(2), time_pass(1)
     wc = W // 2 + 1
@@ -352,6 +387,33 @@ def main():
                "h2d_bytes_per_step": F * CH * H * W * 4, "d2h_bytes_per_step": F * CH * H * W * 4 + (F // G) * 4,
                "ms_per_step": round(ms_e2e, 3), "api": "ils_smooth_host (C ABI), pinned host fp32 planes"}
 
+    # ---- comparison: the same loop on cuFFT + torch elementwise, same frames
+    cufft = None
+    if not args.no_cufft:
+        cpar = params.curvature
+        fg = f[: G * CH * 2]  # two groups per call, like the two lanes
+        with torch.cuda.stream(stream):
+            ref_u = cufft_loop(fg, LAM, ITERS, P_EXP, EPS, cpar)
+            torch.cuda.synchronize()
+            gref = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gref, stream=stream):
+                out_ref = cufft_loop(fg, LAM, ITERS, P_EXP, EPS, cpar)
+            for _ in range(3):
+                gref.replay()
+            reps = max(3, args.steps // 4)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                gref.replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms_ref = max_over_ranks(a.elapsed_time(b) / reps)
+        diff = float((out_ref - u[: fg.shape[0]]).abs().max())
+        cufft = {"value": round(world * (fg.shape[0] // CH) / (ms_ref / 1e3), 2), "unit": "frames/s",
+                 "impl": "torch.fft.rfft2/irfft2 (cuFFT) + torch elementwise, fp32, CUDA graph",
+                 "max_abs_diff_vs_ours": diff}
+        del ref_u
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sec, workers = cpu_port_frame_seconds(frames=1)
@@ -388,6 +450,7 @@ def main():
                                         "frac": round(bpf * value / world / 1e9 / peak, 4),
                                         "bytes_per_frame": bpf}},
             "cpu_baseline": cpu,
+            "cufft_comparison": cufft,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

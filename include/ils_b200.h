@@ -97,9 +97,13 @@ ILS_API ils_status ils_smooth_host(const ils_plan* plan, const void* f_host, voi
                                    int32_t nbatches, void* workspace, void* io_dev, void* stream, int32_t* bad_iter);
 
 /* One pass of the ils_smooth launch sequence on its own (roofline timing and
- * profiling): pass 0 = row pass from f (iteration 0), 1 = column solve pass,
- * 2 = fused row pass (iteration >= 1), 3 = final row pass writing u.  Uses
- * the workspace's first half spectrum as input and output. */
+ * profiling).  pass & 3: 0 = row pass from f (iteration 0), 1 = column solve
+ * pass, 2 = fused row pass (iteration >= 1), 3 = final row pass writing u.
+ * pass & 4 selects which of the workspace's two half spectra is current:
+ * 0 writes spectrum A; 1 solves the current one in place; 2 reads the
+ * current one and writes the other; 3 reads the current one.  The ils_smooth
+ * sequence is therefore 0, 1, 2, 5, 6, 1, 2, 5, ..., ending with 3 or 7
+ * (same results, bit for bit, as ils_smooth). */
 ILS_API ils_status ils_launch_pass(const ils_plan* plan, int32_t pass, const void* f_dev, void* u_dev,
                                    int64_t plane_stride, void* workspace, void* stream, int32_t* status_dev);
 

@@ -863,12 +863,15 @@ ils_status ils_launch_pass(const ils_plan* p, int32_t pass, const void* f, void*
                            void* stream, int32_t* status) {
   if (!p || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
-  if (pass < 0 || pass > 3) return fail(ILS_EINVAL, "pass must be 0..3, got %d", pass);
+  if (pass < 0 || pass > 7 || pass == 4) return fail(ILS_EINVAL, "pass must be 0..3 or 5..7, got %d", pass);
+  const bool second = (pass & 4) != 0;
+  pass &= 3;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto run = [&](auto tag) -> ils_status {
     using T = decltype(tag);
     cx<T>* Sa = static_cast<cx<T>*>(ws);
     cx<T>* Sb = reinterpret_cast<cx<T>*>(static_cast<char*>(ws) + p->spec_bytes);
+    if (second) std::swap(Sa, Sb);
     if (pass == 1) {
       ILS_CUDA(launch_col<T>(p, col_args<T>(p, Sa, COL_SOLVE), s));
       return ILS_OK;

@@ -235,6 +235,38 @@ def test_torch_zero_copy_path_matches_numpy_path():
     assert np.array_equal(u_np, u_t.double().cpu().numpy())
 
 
+@pytest.mark.parametrize("iters", [4, 3])
+def test_launch_pass_sequence_equals_smooth(iters):
+    # the per-pass entry point (roofline timing, bench.py) replays the exact ils_smooth dataflow
+    import ctypes as C
+
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0, iters=iters)
+    f = torch.rand((3, 270, 480), device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    ref = ils.smooth_batch(f, params)
+    plan = rt.get_plan(3, 270, 480, params.c_params(), _lib.ILS_F32, 0)
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+    st = torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device="cuda")
+    u = torch.empty_like(f)
+    order = [0, 1]
+    for n in range(1, iters):
+        cur = 0 if n % 2 else 4
+        order += [2 | cur, 1 | (cur ^ 4)]
+    order += [3 | (0 if iters % 2 else 4)]
+    L = _lib.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for p in order:
+        _lib.check(L.ils_launch_pass(plan.ptr, p, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()), 270 * 480,
+                                     C.c_void_p(ws.data_ptr()), C.c_void_p(s), C.c_void_p(st.data_ptr())),
+                   "ils_launch_pass")
+    torch.cuda.synchronize()
+    assert torch.equal(u, ref)
+    with pytest.raises(ValueError):
+        _lib.check(L.ils_launch_pass(plan.ptr, 4, None, None, 0, C.c_void_p(ws.data_ptr()), C.c_void_p(s),
+                                     C.c_void_p(st.data_ptr())), "ils_launch_pass")
+
+
 # ------------------------------------------------------------ C5 slab decomposition (emulated ranks)
 @pytest.mark.parametrize("H,W,P", [(1080, 1920, 2), (1080, 1920, 3), (256, 320, 4), (90, 128, 8)])
 def test_slab_decomposition_bitwise_equals_single_gpu(H, W, P):
