@@ -41,7 +41,7 @@ typedef enum {
   ILS_EUNSUPPORTED = 5      /* a side has a prime factor > 61 -> ValueError */
 } ils_status;
 
-typedef enum { ILS_CHARBONNIER = 0, ILS_WELSCH = 1 } ils_penalty_kind;
+typedef enum { ILS_CHARBONNIER = 0, ILS_WELSCH = 1, ILS_SOFT = 2 /* HQS plans only */ } ils_penalty_kind;
 typedef enum { ILS_F32 = 0, ILS_F64 = 1 } ils_dtype;
 
 /* Value of a device status word that saw no failure (memset pattern 0x7f). */
@@ -68,6 +68,22 @@ typedef struct ils_plan ils_plan;
 ILS_API ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_t width, const ils_params* params,
                            int32_t dtype, int32_t device);
 ILS_API void ils_plan_destroy(ils_plan* plan);
+
+/* HqsParams (hqs.py:27-47): the penalty-splitting baseline for the L1
+ * gradient objective.  beta0 = 0 selects the default 2*lam.  A plan from
+ * ils_hqs_plan_create runs hqs_smooth_plane (hqs.py:50-66) through
+ * ils_smooth / ils_smooth_host: per iteration n the field step
+ * m = soft_threshold(grad u, lam / (2 beta_n)) is fused into the row pass
+ * and the u-step solve_ls(lam = 2 beta_n, c = 1) uses the per-iteration
+ * denominator 1 + beta_n (wy + wx), beta_n = beta0 kappa^n.  No energy trace. */
+typedef struct {
+  double lam;    /* > 0, finite */
+  double beta0;  /* > 0 finite, or 0 for 2*lam */
+  double kappa;  /* > 1, finite */
+  int32_t iters; /* >= 1 */
+} ils_hqs_params;
+ILS_API ils_status ils_hqs_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_t width,
+                                       const ils_hqs_params* params, int32_t dtype, int32_t device);
 
 /* Bytes of device workspace one in-flight ils_smooth/ils_solve_ls call needs
  * (two half spectra + trace partials).  One workspace per concurrent call. */

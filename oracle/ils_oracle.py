@@ -186,6 +186,32 @@ def smooth_plane(f, spec, lam, iters=4, c=None, trace=False, workers=1):
     return (u, energies) if trace else u
 
 
+# ---------------------------------------------------------------- HQS baseline
+def soft_threshold(x, alpha):
+    """penalty.py:168-177."""
+    x = np.asarray(x, dtype=np.float64)
+    return np.where(np.abs(x) <= alpha, 0.0, x - alpha * np.sign(x))
+
+
+def hqs_smooth_plane(f, lam, beta0=None, kappa=2.0, iters=4, workers=1):
+    """hqs.py:50-66: beta_n = beta0 kappa^n, alpha_n = lam / (2 beta_n),
+    m = soft_threshold(grad u, alpha_n), u = solve_ls(lam=2 beta_n, c=1)."""
+    f = np.asarray(f, dtype=np.float64)
+    h, w = f.shape
+    beta = 2.0 * lam if beta0 is None else float(beta0)  # HqsParams.initial_beta, hqs.py:45-47
+    f_hat = _sfft.fft2(f, workers=workers)  # hqs.py:52-53
+    u = f
+    for n in range(iters):
+        b = beta * kappa ** n
+        alpha = lam / (2.0 * b)
+        mx = soft_threshold(grad_x(u), alpha)
+        my = soft_threshold(grad_y(u), alpha)
+        u = solve_ls(f, mx, my, 2.0 * b, 1.0, workers, f_hat=f_hat, denom=denominator(h, w, 2.0 * b, 1.0))
+        if not np.all(np.isfinite(u)):
+            raise ArithmeticError(f"non-finite iterate at iteration {n + 1}")
+    return u
+
+
 def rgb_to_yuv(r, g, b):
     """image.py:110-117 (BT.601)."""
     y = 0.299 * r + 0.587 * g + 0.114 * b

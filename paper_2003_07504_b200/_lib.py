@@ -17,12 +17,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libils_b200.so")
 
 ILS_OK, ILS_EINVAL, ILS_ENONFINITE_INPUT, ILS_ENONFINITE, ILS_ECUDA, ILS_EUNSUPPORTED = range(6)
-ILS_CHARBONNIER, ILS_WELSCH = 0, 1
+ILS_CHARBONNIER, ILS_WELSCH, ILS_SOFT = 0, 1, 2
 ILS_F32, ILS_F64 = 0, 1
 STATUS_CLEAN = 0x7F7F7F7F
 
 EXPORTS = (
-    "ils_plan_create", "ils_plan_destroy", "ils_workspace_size", "ils_smooth", "ils_smooth_host",
+    "ils_plan_create", "ils_hqs_plan_create", "ils_plan_destroy", "ils_workspace_size", "ils_smooth", "ils_smooth_host",
     "ils_host_io_size", "ils_launch_pass", "ils_slab_plan_create", "ils_slab_get_layout", "ils_slab_row_pass",
     "ils_slab_col_pass",
     "ils_solve_ls", "ils_rfft2", "ils_irfft2", "ils_rgb_yuv", "ils_plan_get_info", "ils_last_error",
@@ -33,6 +33,10 @@ EXPORTS = (
 class Params(C.Structure):
     _fields_ = [("kind", C.c_int32), ("p", C.c_double), ("eps", C.c_double), ("gamma", C.c_double),
                 ("lam", C.c_double), ("c", C.c_double), ("iters", C.c_int32)]
+
+
+class HqsParams(C.Structure):
+    _fields_ = [("lam", C.c_double), ("beta0", C.c_double), ("kappa", C.c_double), ("iters", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -58,6 +62,8 @@ _P = C.c_void_p
 _SIGS = {
     "ils_plan_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, C.c_int32, C.POINTER(Params), C.c_int32,
                                   C.c_int32]),
+    "ils_hqs_plan_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, C.c_int32, C.POINTER(HqsParams),
+                                      C.c_int32, C.c_int32]),
     "ils_plan_destroy": (None, [_P]),
     "ils_workspace_size": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
     "ils_smooth": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, _P, _P]),

@@ -60,8 +60,12 @@ class DevicePlan:
     def __init__(self, batch, height, width, cparams, dtype_code, device_index):
         L = _lib.lib()
         h = C.c_void_p()
-        _lib.check(L.ils_plan_create(C.byref(h), batch, height, width, C.byref(cparams), dtype_code, device_index),
-                   "ils_plan_create")
+        if isinstance(cparams, _lib.HqsParams):  # penalty-splitting baseline (hqs.py)
+            _lib.check(L.ils_hqs_plan_create(C.byref(h), batch, height, width, C.byref(cparams), dtype_code,
+                                             device_index), "ils_hqs_plan_create")
+        else:
+            _lib.check(L.ils_plan_create(C.byref(h), batch, height, width, C.byref(cparams), dtype_code,
+                                         device_index), "ils_plan_create")
         self.ptr = h
         self.batch, self.height, self.width = batch, height, width
         self.dtype_code = dtype_code
@@ -83,8 +87,8 @@ class DevicePlan:
 
 
 def get_plan(batch, height, width, cparams, dtype_code, device_index) -> DevicePlan:
-    key = (batch, height, width, cparams.kind, cparams.p, cparams.eps, cparams.gamma, cparams.lam, cparams.c,
-           cparams.iters, dtype_code, device_index)
+    key = (batch, height, width, type(cparams).__name__) + tuple(getattr(cparams, n) for n, _ in cparams._fields_) + (
+        dtype_code, device_index)
     with _plans_lock:
         plan = _plans.get(key)
         if plan is None:

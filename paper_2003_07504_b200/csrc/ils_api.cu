@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -267,6 +268,8 @@ struct ils_plan {
   int P = 1, rank = 0;
   int row0[kMaxSeg + 1] = {0}, col0[kMaxSeg + 1] = {0}, pitch[kMaxSeg] = {0};
   int Hl = 0, Wcl = 0;  // local rows, local spectrum columns
+  // penalty-splitting baseline (ils_hqs_plan_create): beta_n = beta0 kappa^n
+  double hqs_beta0 = 0, hqs_kappa = 0;
 };
 
 namespace {
@@ -426,10 +429,31 @@ PenaltyDev<T> pen_dev(const ils_params& q) {
   P.eps0 = q.kind == ILS_CHARBONNIER ? T(q.eps) : T(0);
   P.E = q.kind == ILS_CHARBONNIER ? T(q.p / 2.0 - 1.0) : P.wk;
   P.coef = q.kind == ILS_CHARBONNIER ? T(-q.p) : T(-2.0);
+  P.floor = -std::numeric_limits<T>::infinity();
   P.g2x2 = T(2.0 * g2);
   P.c = T(q.c);
   P.lam = T(q.lam);
   P.lam2 = T(q.lam / 2.0);
+  return P;
+}
+
+// HQS iteration n (hqs.py:49-66): field step m = soft_threshold(grad u, alpha)
+// with alpha = lam / (2 beta_n), then solve_ls with lam_n = 2 beta_n, c = 1,
+// i.e. rhs = f + beta_n D^T m and denominator 1 + beta_n (wy + wx).  The soft
+// threshold is the penalty form mu = x max(1 - alpha |x|^-1, 0).
+double hqs_beta(const ils_plan* p, int n) { return p->hqs_beta0 * std::pow(p->hqs_kappa, n); }
+
+template <typename T>
+PenaltyDev<T> pen_soft(double alpha, double beta) {
+  PenaltyDev<T> P{};
+  P.kind = ILS_SOFT;
+  P.eps0 = T(0);
+  P.E = T(-0.5);
+  P.coef = T(-alpha);
+  P.c = T(1);
+  P.floor = T(0);
+  P.lam = T(2.0 * beta);
+  P.lam2 = T(beta);
   return P;
 }
 
@@ -528,14 +552,18 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
   const int iters = p->prm.iters;
   cx<T>* cur = Sa;
   cx<T>* nxt = Sb;
+  const bool hqs = p->prm.kind == ILS_SOFT;
   for (int n = 0; n < iters; ++n) {
     a.iter = n;
     a.Sin = n == 0 ? nullptr : cur;
     a.Sout = n == 0 ? cur : nxt;
     a.epart = energies ? ep + n * per_pass : nullptr;
+    if (hqs) a.pen = pen_soft<T>(p->prm.lam / (2.0 * hqs_beta(p, n)), hqs_beta(p, n));
     ILS_CUDA(launch_row<T>(p, n == 0 ? MODE_F0 : MODE_IT, a, s));
     if (n > 0) std::swap(cur, nxt);
-    ILS_CUDA(launch_col<T>(p, col_args<T>(p, cur, COL_SOLVE), s));
+    ColArgs<T> ca = col_args<T>(p, cur, COL_SOLVE);
+    if (hqs) ca.cl2 = T(hqs_beta(p, n));
+    ILS_CUDA(launch_col<T>(p, ca, s));
   }
   a.iter = iters;
   a.Sin = cur;
@@ -577,6 +605,9 @@ ils_status solve_t(const ils_plan* p, const T* f, const T* mx, const T* my, T* u
   return ILS_OK;
 }
 
+ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32_t width, const ils_params* params,
+                            int32_t dtype, int32_t device, double hqs_beta0, double hqs_kappa);
+
 ils_status validate(const ils_params* q) {
   if (!q) return fail(ILS_EINVAL, "params is NULL");
   if (!(q->lam > 0.0 && std::isfinite(q->lam))) return fail(ILS_EINVAL, "lam must be finite and positive, got %g", q->lam);
@@ -608,11 +639,40 @@ ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_
                            int32_t dtype, int32_t device) {
   if (!out) return fail(ILS_EINVAL, "out is NULL");
   *out = nullptr;
+  ils_status st = validate(params);
+  if (st != ILS_OK) return st;
+  return plan_create_impl(out, batch, height, width, params, dtype, device, 0.0, 0.0);
+}
+
+ils_status ils_hqs_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_t width,
+                               const ils_hqs_params* hp, int32_t dtype, int32_t device) {
+  if (!out) return fail(ILS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!hp) return fail(ILS_EINVAL, "params is NULL");
+  // HqsParams.__post_init__ (hqs.py:33-43)
+  if (!(hp->lam > 0.0 && std::isfinite(hp->lam))) return fail(ILS_EINVAL, "lam must be finite and positive, got %g", hp->lam);
+  if (hp->beta0 != 0.0 && !(hp->beta0 > 0.0 && std::isfinite(hp->beta0)))
+    return fail(ILS_EINVAL, "beta0 must be finite and positive, got %g", hp->beta0);
+  if (!(hp->kappa > 1.0 && std::isfinite(hp->kappa))) return fail(ILS_EINVAL, "kappa must be finite and > 1, got %g", hp->kappa);
+  if (hp->iters < 1) return fail(ILS_EINVAL, "iters must be an integer >= 1, got %d", hp->iters);
+  ils_params q{};
+  q.kind = ILS_SOFT;
+  q.lam = hp->lam;
+  q.c = 1.0;
+  q.iters = hp->iters;
+  const double beta0 = hp->beta0 == 0.0 ? 2.0 * hp->lam : hp->beta0;  // HqsParams.initial_beta (hqs.py:45-47)
+  return plan_create_impl(out, batch, height, width, &q, dtype, device, beta0, hp->kappa);
+}
+
+}  // extern "C"
+
+namespace {
+
+ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32_t width, const ils_params* params,
+                            int32_t dtype, int32_t device, double hqs_beta0, double hqs_kappa) {
   if (batch < 1) return fail(ILS_EINVAL, "batch must be >= 1, got %d", batch);
   if (height < 1 || width < 1) return fail(ILS_EINVAL, "invalid plan size %dx%d", height, width);
   if (dtype != ILS_F32 && dtype != ILS_F64) return fail(ILS_EINVAL, "unknown dtype %d", dtype);
-  ils_status st = validate(params);
-  if (st != ILS_OK) return st;
   if (has_big_prime(height) || has_big_prime(width % 2 == 0 ? width / 2 : width))
     return fail(ILS_EUNSUPPORTED, "plane size %dx%d has a prime factor > %d (unsupported FFT length)", height, width,
                 kMaxGenericPrime);
@@ -627,6 +687,8 @@ ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_
   p->dtype = dtype;
   p->device = device;
   p->prm = *params;
+  p->hqs_beta0 = hqs_beta0;
+  p->hqs_kappa = hqs_kappa;
   const size_t elt = dtype == ILS_F32 ? sizeof(cx<float>) : sizeof(cx<double>);
   const int maxe = dtype == ILS_F32 ? 16 : 8;
   if (device >= 0) {
@@ -699,6 +761,10 @@ ils_status ils_plan_create(ils_plan** out, int32_t batch, int32_t height, int32_
   return ILS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 void ils_plan_destroy(ils_plan* p) {
   if (!p) return;
   if (p->d_tables) cudaFree(p->d_tables);
@@ -748,6 +814,7 @@ ils_status ils_smooth(const ils_plan* p, const void* f, void* u, int64_t ps, voi
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (p->slab) return fail(ILS_EINVAL, "slab plans run through ils_slab_row_pass / ils_slab_col_pass");
   if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
+  if (energies && p->prm.kind == ILS_SOFT) return fail(ILS_EINVAL, "the penalty-splitting baseline has no energy trace");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
     return smooth_t<float>(p, static_cast<const float*>(f), static_cast<float*>(u), ps, ws, s, status, energies);

@@ -36,7 +36,7 @@ constexpr int kMaxBandLines = 32;        // band + 2 halo lines per row CTA (mba
 
 template <typename T>
 struct PenaltyDev {
-  int kind;   // 0 Charbonnier, 1 Welsch
+  int kind;   // 0 Charbonnier, 1 Welsch, 2 soft threshold (HQS field step)
   T p;        // Charbonnier exponent
   T pe;       // p/2 - 1
   T ph;       // p/2
@@ -46,9 +46,11 @@ struct PenaltyDev {
   T c;        // curvature
   T lam;
   T lam2;     // lam / 2
-  // branch-free mu = x * (c + coef * 2^(E * Lg)), Lg = log2(x^2 + eps0)
-  // (Charbonnier) or x^2 (Welsch): one code path for both families
-  T eps0, E, coef;
+  // branch-free mu = x * max(c + coef * 2^(E * Lg), floor), Lg = log2(x^2 + eps0)
+  // (Charbonnier, soft threshold) or x^2 (Welsch): one code path for all
+  // three.  floor = -inf for the ILS penalties (c >= c0 keeps the factor
+  // >= 0 anyway); 0 for the soft threshold x * max(1 - alpha/|x|, 0).
+  T eps0, E, coef, floor;
 };
 
 constexpr int kMaxSeg = 8;  // ranks of a slab-decomposed (distributed) transform
@@ -142,9 +144,9 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 template <typename T>
 __device__ __forceinline__ T aux(T x, const PenaltyDev<T>& P) {
   const T q = fma_rn(x, x, P.eps0);
-  const T lg = P.kind == 0 ? lg2_(q) : q;
+  const T lg = P.kind != 1 ? lg2_(q) : q;
   const T t = ex2_(mul_rn(P.E, lg));
-  return mul_rn(x, fma_rn(P.coef, t, P.c));
+  return mul_rn(x, fmax(fma_rn(P.coef, t, P.c), P.floor));
 }
 // phi(x): penalty.py:60-62, 88-91 (energy trace only)
 template <typename T>
@@ -759,7 +761,7 @@ constexpr int kColBlocksOf = FS::ME > 16 ? 2 : kColMinBlocks;
 
 template <typename T, class FS>
 __global__ void __launch_bounds__(kColThreads, kColBlocksOf<FS>) k_col(const ColArgs<T> A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
   T* swy = reinterpret_cast<T*>(tile + A.C * A.CS);  // wy[0..H) staged once per CTA
   using Grp = GroupT<FS::G>;

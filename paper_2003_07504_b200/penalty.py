@@ -87,6 +87,22 @@ def check_curvature(spec, c: float) -> None:
         )
 
 
+def soft_threshold(x, alpha: float):
+    """penalty.py:168-177 (host helper; the HQS field step runs fused in the row kernel)."""
+    if not (alpha >= 0.0 and np.isfinite(alpha)):
+        raise ValueError(f"alpha must be finite and >= 0, got {alpha}")
+    x = np.asarray(x, dtype=np.float64)
+    return np.where(np.abs(x) <= alpha, 0.0, x - alpha * np.sign(x))
+
+
+def huber(x, alpha: float):
+    """penalty.py:180-191 (host helper)."""
+    if not (alpha > 0.0 and np.isfinite(alpha)):
+        raise ValueError(f"alpha must be finite and > 0, got {alpha}")
+    x = np.asarray(x, dtype=np.float64)
+    return np.where(np.abs(x) <= alpha, x * x / (2.0 * alpha), np.abs(x) - alpha / 2.0)
+
+
 def to_c_params(spec, lam: float, c: float, iters: int):
     """Flatten (penalty, lam, c, iters) into the C ABI's ils_params."""
     from ._lib import ILS_CHARBONNIER, ILS_WELSCH, Params

@@ -89,6 +89,23 @@ def main():
     g["c1_rows"] = u[[0, 1, 255, 511], :]  # four full rows for pointwise checks
     g["c1_cols"] = u[:, [0, 7, 300, 511]]
 
+    # --- HQS penalty-splitting baseline (hqs.py:50-66; test_hqs.py cases + sizes the FFT plans care about)
+    clean = np.full((32, 32), 0.25)
+    clean[:, 16:] = 0.75
+    noisy = np.clip(clean + 0.05 * np.random.default_rng(4).standard_normal((32, 32)), 0.0, 1.0)
+    hqs_cases = [
+        ("hqs_sched_20x16", np.random.default_rng(2).random((20, 16)), 0.25, None, 2.0, 4),
+        ("hqs_noise_32x32", noisy, 0.25, None, 2.0, 4),
+        ("hqs_beta_33x45", np.random.default_rng(21).random((33, 45)), 0.1, 0.5, 1.5, 6),
+        ("hqs_prime_17x13", np.random.default_rng(22).random((17, 13)), 1.0, None, 3.0, 3),
+        ("hqs_card_96x128", np.random.default_rng(23).random((96, 128)), 0.05, None, 2.0, 5),
+    ]
+    for name, f, lam, beta0, kappa, iters in hqs_cases:
+        u = ref.hqs_smooth_plane(f, ref.HqsParams(lam, beta0=beta0, kappa=kappa, iters=iters))
+        g[name + "_f"] = f
+        g[name + "_u"] = u
+        g[name + "_prm"] = np.array([lam, -1.0 if beta0 is None else beta0, kappa, iters])
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 

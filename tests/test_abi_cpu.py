@@ -21,7 +21,7 @@ def _header_symbols():
 def test_library_loads_and_exports_every_header_symbol():
     L = _lib.lib()
     syms = _header_symbols()
-    assert len(syms) == 18
+    assert len(syms) == 19
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
@@ -172,3 +172,30 @@ def test_no_cpu_fallback_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         ils.smooth_plane(np.zeros((8, 8)), ils.SmoothParams(ils.Charbonnier(0.8), 1.0))
+
+
+def test_hqs_params_validation_matches_reference():
+    # hqs.py:33-43 (HqsParams) and the C ABI's own checks (host-only plans, no GPU)
+    import ctypes as C
+
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib
+
+    for bad in (dict(lam=0.0), dict(lam=1.0, beta0=-1.0), dict(lam=1.0, kappa=1.0), dict(lam=1.0, iters=0)):
+        with pytest.raises(ValueError):
+            ils.HqsParams(**bad)
+    assert ils.HqsParams(0.25).initial_beta == 0.5
+    assert ils.HqsParams(0.25, beta0=3.0).initial_beta == 3.0
+    L = _lib.lib()
+    h = C.c_void_p()
+    ok = _lib.HqsParams(0.25, 0.0, 2.0, 4)
+    _lib.check(L.ils_hqs_plan_create(C.byref(h), 3, 1080, 1920, C.byref(ok), _lib.ILS_F32, -1), "create")
+    L.ils_plan_destroy(h)
+    for bad in (_lib.HqsParams(0.0, 0.0, 2.0, 4), _lib.HqsParams(1.0, -2.0, 2.0, 4), _lib.HqsParams(1.0, 0.0, 1.0, 4),
+                _lib.HqsParams(1.0, 0.0, 2.0, 0), _lib.HqsParams(float("inf"), 0.0, 2.0, 4)):
+        with pytest.raises(ValueError):
+            _lib.check(L.ils_hqs_plan_create(C.byref(h), 1, 8, 8, C.byref(bad), _lib.ILS_F32, -1), "create")
+    # the soft-threshold kind is not an ILS penalty: ils_plan_create refuses it
+    p = _lib.Params(_lib.ILS_SOFT, 0.0, 0.0, 0.0, 1.0, 1.0, 4)
+    with pytest.raises(ValueError):
+        _lib.check(L.ils_plan_create(C.byref(h), 1, 8, 8, C.byref(p), _lib.ILS_F32, -1), "create")

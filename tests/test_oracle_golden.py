@@ -110,3 +110,27 @@ def test_golden_energy_trace_csv():
         assert f"{en[i]:.12g}" == row["energy"], i
         rel = 1.0 if e0 == elast else (e0 - en[i]) / (e0 - elast)
         assert f"{rel:.12g}" == row["rel_decrease"], i
+
+
+def _hqs_cases(g):
+    return sorted({k[: -len("_prm")] for k in g.files if k.startswith("hqs_") and k.endswith("_prm")})
+
+
+def test_hqs_matches_reference_goldens(g):
+    # hqs.py:50-66 via tests/golden/make_golden.py (test_hqs.py inputs + extra sizes/schedules)
+    names = _hqs_cases(g)
+    assert len(names) == 5
+    for name in names:
+        lam, beta0, kappa, iters = g[name + "_prm"]
+        u = O.hqs_smooth_plane(g[name + "_f"], lam, None if beta0 < 0 else beta0, kappa, int(iters))
+        assert np.max(np.abs(u - g[name + "_u"])) < 1e-12, name
+
+
+def test_hqs_field_step_is_grid_optimal():
+    # pkg/tests/test_hqs.py:34-46 restated on the oracle's soft threshold
+    rng = np.random.default_rng(0)
+    grid = np.linspace(-3.0, 3.0, 12001)
+    for _ in range(40):
+        x, beta, lam = rng.uniform(-2, 2), rng.uniform(0.1, 5.0), rng.uniform(0.05, 2.0)
+        m = float(O.soft_threshold(x, lam / (2 * beta)))
+        assert beta * (x - m) ** 2 + lam * abs(m) <= float((beta * (x - grid) ** 2 + lam * np.abs(grid)).min()) + 1e-7
