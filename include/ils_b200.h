@@ -112,6 +112,21 @@ ILS_API ils_status ils_host_io_size(const ils_plan* plan, size_t* bytes);
 ILS_API ils_status ils_smooth_host(const ils_plan* plan, const void* f_host, void* u_host, int64_t plane_stride,
                                    int32_t nbatches, void* workspace, void* io_dev, void* stream, int32_t* bad_iter);
 
+/* 8-bit interleaved frames, the reference's PNG/PPM pixel path fused into
+ * the first and last passes (formats.py:25-27 read v/255, write
+ * floor(clip01(u)*255 + 0.5); image.py MultiImage.from_array channel split).
+ * f_dev / u_dev: frames [batch/channels][H][W][channels] bytes on the plan's
+ * device; plan batch = frames * channels.  Same result as smoothing the
+ * planes v/255 with ils_smooth and quantising u.  No energy trace. */
+ILS_API ils_status ils_smooth_u8(const ils_plan* plan, const uint8_t* f_dev, uint8_t* u_dev, int32_t channels,
+                                 void* workspace, void* stream, int32_t* status_dev);
+/* ils_smooth_host for 8-bit frames: nbatches consecutive batches of
+ * batch/channels frames, pipelined as ils_smooth_host (io_dev:
+ * ils_host_io_size bytes). */
+ILS_API ils_status ils_smooth_host_u8(const ils_plan* plan, const uint8_t* f_host, uint8_t* u_host, int32_t channels,
+                                      int32_t nbatches, void* workspace, void* io_dev, void* stream,
+                                      int32_t* bad_iter);
+
 /* One pass of the ils_smooth launch sequence on its own (roofline timing and
  * profiling).  pass & 3: 0 = row pass from f (iteration 0), 1 = column solve
  * pass, 2 = fused row pass (iteration >= 1), 3 = final row pass writing u.

@@ -186,6 +186,22 @@ def smooth_plane(f, spec, lam, iters=4, c=None, trace=False, workers=1):
     return (u, energies) if trace else u
 
 
+# ---------------------------------------------------------------- 8-bit I/O
+def quantize(plane):
+    """formats.py:25-27: floor(clip01(v) * 255 + 0.5) as uint8 (image.clip01 = np.clip(v, 0, 1))."""
+    return np.floor(np.clip(plane, 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+
+
+def smooth_u8(arr, spec, lam, iters=4, c=None, workers=1):
+    """8-bit image [H, W] or [H, W, C] -> the reference's PNG round trip:
+    arr / 255 (formats.py:43) -> smooth per channel -> quantize (formats.py:54-59)."""
+    f = np.asarray(arr, dtype=np.float64) / 255.0
+    if f.ndim == 2:
+        return quantize(smooth_plane(f, spec, lam, iters, c, workers=workers))
+    return np.stack([quantize(smooth_plane(f[..., k], spec, lam, iters, c, workers=workers))
+                     for k in range(f.shape[-1])], axis=-1)
+
+
 # ---------------------------------------------------------------- HQS baseline
 def soft_threshold(x, alpha):
     """penalty.py:168-177."""

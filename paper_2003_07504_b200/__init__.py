@@ -12,7 +12,7 @@ from .errors import ImageFormatError, NumericalError
 from .image import GRAY, RGB, YUV, ColorMode, MultiImage, as_plane, rgb_to_yuv, yuv_to_rgb
 from .hqs import HqsParams, hqs_smooth_batch, hqs_smooth_plane
 from .penalty import DEFAULT_EPS, Charbonnier, Welsch, check_curvature, huber, soft_threshold
-from .smoother import EnergyTrace, SmoothParams, smooth_batch, smooth_color, smooth_plane
+from .smoother import EnergyTrace, SmoothParams, smooth_batch, smooth_color, smooth_frames_u8, smooth_plane
 from .solver import SolverPlan, make_plan, solve_ls
 
 __version__ = "0.1.0"
@@ -20,6 +20,6 @@ __version__ = "0.1.0"
 __all__ = [
     "DEFAULT_EPS", "GRAY", "RGB", "YUV", "Charbonnier", "ColorMode", "EnergyTrace", "HqsParams", "ImageFormatError",
     "MultiImage", "NumericalError", "SmoothParams", "SolverPlan", "Welsch", "as_plane", "check_curvature",
-    "get_default_precision", "hqs_smooth_batch", "hqs_smooth_plane", "huber", "make_plan", "rgb_to_yuv", "set_default_precision", "smooth_batch", "smooth_color",
+    "get_default_precision", "hqs_smooth_batch", "hqs_smooth_plane", "huber", "make_plan", "rgb_to_yuv", "set_default_precision", "smooth_batch", "smooth_color", "smooth_frames_u8",
     "smooth_plane", "soft_threshold", "solve_ls", "yuv_to_rgb",
 ]

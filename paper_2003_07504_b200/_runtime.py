@@ -223,3 +223,29 @@ def to_device_planes(planes, precision=None):
 def to_host_f64(t):
     arr = t.detach().to("cpu").to(dtype=_torch().float64).numpy()
     return [np.ascontiguousarray(arr[i]) for i in range(arr.shape[0])]
+
+
+def smooth_device_u8(frames, cparams, precision=None, check=True):
+    """8-bit interleaved frames uint8[F, H, W, C] on the GPU -> same layout (ils_smooth_u8).
+
+    Equals quantising (floor(clip01(u) 255 + 0.5), formats.py:25-27) the
+    smoothing of the planes v / 255 (formats.py read side); the conversions
+    run inside the first and last row passes.
+    """
+    torch = _torch()
+    if frames.dim() != 4 or not frames.is_cuda or frames.dtype != torch.uint8:
+        raise ValueError("smooth_device_u8 expects a CUDA uint8 tensor [F, H, W, C]")
+    frames = frames.contiguous()
+    F, H, W, Ch = frames.shape
+    code = _lib.ILS_F32 if (precision or _PRECISION) == "fp32" else _lib.ILS_F64
+    dev = frames.device
+    plan = get_plan(F * Ch, H, W, cparams, code, dev.index if dev.index is not None else torch.cuda.current_device())
+    u = torch.empty_like(frames)
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().ils_smooth_u8(plan.ptr, C.c_void_p(frames.data_ptr()), C.c_void_p(u.data_ptr()), Ch,
+                                        C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev),
+                                        C.c_void_p(status.data_ptr())), "ils_smooth_u8")
+    if check:
+        raise_status(int(status.item()))
+    return u

@@ -262,6 +262,7 @@ struct ils_plan {
   void* d_tables = nullptr;
   size_t off_rowtw, off_coltw, off_wreal, off_wx, off_wy, off_sink;  // byte offsets
   size_t spec_bytes;                                       // one half spectrum
+  size_t off_fcopy;                                        // workspace: planar f of the 8-bit path
   size_t epart_elems;                                      // doubles for trace partials
   // slab decomposition (ils_slab_plan_create): this rank's rows / columns
   bool slab = false;
@@ -533,9 +534,11 @@ cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
   return launch_col_impl<T, FftRt>(a, grid, p->col_threads, p->col_smem, s);
 }
 
+// f8 / u8 (8-bit interleaved frames, ch channels): F0 reads f8 and keeps a
+// planar copy of f in the workspace for the later passes; FIN writes u8.
 template <typename T>
 ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, cudaStream_t s, int32_t* status,
-                    double* energies) {
+                    double* energies, const unsigned char* f8 = nullptr, unsigned char* u8 = nullptr, int ch = 1) {
   cx<T>* Sa = static_cast<cx<T>*>(ws);
   cx<T>* Sb = reinterpret_cast<cx<T>*>(static_cast<char*>(ws) + p->spec_bytes);
   double* ep = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * p->spec_bytes + 256);
@@ -549,6 +552,13 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
   a.u_ps = ps;
   a.u_rp = p->W;
   a.status = status;
+  if (f8) {
+    a.f8 = f8;
+    a.ch = ch;
+    a.fcopy = reinterpret_cast<T*>(static_cast<char*>(ws) + p->off_fcopy);
+    a.f = a.fcopy;
+    a.f_ps = (int64_t)p->H * p->W;
+  }
   const int iters = p->prm.iters;
   cx<T>* cur = Sa;
   cx<T>* nxt = Sb;
@@ -560,6 +570,7 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
     a.epart = energies ? ep + n * per_pass : nullptr;
     if (hqs) a.pen = pen_soft<T>(p->prm.lam / (2.0 * hqs_beta(p, n)), hqs_beta(p, n));
     ILS_CUDA(launch_row<T>(p, n == 0 ? MODE_F0 : MODE_IT, a, s));
+    a.f8 = nullptr;
     if (n > 0) std::swap(cur, nxt);
     ColArgs<T> ca = col_args<T>(p, cur, COL_SOLVE);
     if (hqs) ca.cl2 = T(hqs_beta(p, n));
@@ -569,6 +580,8 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
   a.Sin = cur;
   a.Sout = nullptr;
   a.epart = energies ? ep + iters * per_pass : nullptr;
+  a.u8 = u8;
+  a.ch = ch;
   ILS_CUDA(launch_row<T>(p, MODE_FIN, a, s));
   if (energies) {
     for (int n = 0; n <= iters; ++n) {
@@ -742,6 +755,7 @@ ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32
   put(p->off_wy, wy);
   p->spec_bytes = ((size_t)batch * height * p->Sp * elt + 255) & ~size_t(255);
   p->epart_elems = (size_t)(params->iters + 1) * batch * p->row_grid;
+  p->off_fcopy = (2 * p->spec_bytes + 256 + p->epart_elems * sizeof(double) + 255) & ~size_t(255);
   if (device < 0) {  // host-only plan: planning/introspection, cannot run
     *out = p;
     return ILS_OK;
@@ -773,7 +787,8 @@ void ils_plan_destroy(ils_plan* p) {
 
 ils_status ils_workspace_size(const ils_plan* p, size_t* bytes) {
   if (!p || !bytes) return fail(ILS_EINVAL, "NULL argument");
-  *bytes = 2 * p->spec_bytes + 256 + p->epart_elems * sizeof(double);  // [Sa][Sb][status][trace partials]
+  // [Sa][Sb][status][trace partials][planar f of the 8-bit path]
+  *bytes = p->off_fcopy + (size_t)p->B * p->H * p->W * (p->dtype == ILS_F32 ? 4 : 8);
   return ILS_OK;
 }
 
@@ -821,6 +836,20 @@ ils_status ils_smooth(const ils_plan* p, const void* f, void* u, int64_t ps, voi
   return smooth_t<double>(p, static_cast<const double*>(f), static_cast<double*>(u), ps, ws, s, status, energies);
 }
 
+ils_status ils_smooth_u8(const ils_plan* p, const uint8_t* f, uint8_t* u, int32_t channels, void* ws, void* stream,
+                         int32_t* status) {
+  if (!p || !f || !u || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (p->slab) return fail(ILS_EINVAL, "slab plans run through ils_slab_row_pass / ils_slab_col_pass");
+  if (channels < 1 || p->B % channels != 0)
+    return fail(ILS_EINVAL, "plan batch %d is not a whole number of %d-channel frames", p->B, channels);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t ps = (int64_t)p->H * p->W;
+  if (p->dtype == ILS_F32)
+    return smooth_t<float>(p, nullptr, nullptr, ps, ws, s, status, nullptr, f, u, channels);
+  return smooth_t<double>(p, nullptr, nullptr, ps, ws, s, status, nullptr, f, u, channels);
+}
+
 ils_status ils_solve_ls(const ils_plan* p, const void* f, const void* mx, const void* my, void* u, int64_t ps,
                         void* ws, void* stream, int32_t* status) {
   if (!p || !f || !mx || !my || !u || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
@@ -842,20 +871,24 @@ ils_status ils_host_io_size(const ils_plan* p, size_t* bytes) {
   return ILS_OK;
 }
 
-ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, int64_t ps, int32_t nbatches,
-                           void* ws, void* io_dev, void* stream, int32_t* bad_iter) {
-  if (!p || !f_host || !u_host || !ws || !io_dev) return fail(ILS_EINVAL, "NULL argument");
-  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
-  if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
-  if (ps != (int64_t)p->H * p->W) return fail(ILS_EINVAL, "host planes must be dense (plane_stride == H*W)");
+}  // extern "C"
+
+namespace {
+
+// Pipelined host path shared by ils_smooth_host / ils_smooth_host_u8: batch k's
+// host->device copy and batch k-1's device->host copy overlap batch k's
+// kernels (two I/O slots, three streams).  run(f_dev, u_dev, status_dev)
+// enqueues one batch on the caller's stream.
+template <class Run>
+ils_status host_pipeline(const void* f_host, void* u_host, size_t in_bytes, size_t out_bytes, int32_t nbatches,
+                         void* io_dev, void* stream, int32_t* bad_iter, Run run) {
   if (bad_iter) *bad_iter = -1;
-  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
-  const size_t bytes = (size_t)p->B * ps * es;
-  const size_t slot = (bytes + 255) & ~size_t(255);
+  const size_t slot_in = (in_bytes + 255) & ~size_t(255), slot_out = (out_bytes + 255) & ~size_t(255);
   char* io = static_cast<char*>(io_dev);
-  char* fslot[2] = {io, io + slot};
-  char* uslot[2] = {io + 2 * slot, io + 3 * slot};
-  int32_t* st[2] = {reinterpret_cast<int32_t*>(io + 4 * slot), reinterpret_cast<int32_t*>(io + 4 * slot + 128)};
+  char* fslot[2] = {io, io + slot_in};
+  char* uslot[2] = {io + 2 * slot_in, io + 2 * slot_in + slot_out};
+  char* stw = io + 2 * slot_in + 2 * slot_out;
+  int32_t* st[2] = {reinterpret_cast<int32_t*>(stw), reinterpret_cast<int32_t*>(stw + 128)};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
@@ -894,21 +927,21 @@ ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, 
   ILS_TRY(cudaStreamWaitEvent(d2h, ev_out[0], 0));
   for (int k = 0; k < nbatches; ++k) {
     const int sl = k & 1;
-    const char* fh = static_cast<const char*>(f_host) + (size_t)k * bytes;
-    char* uh = static_cast<char*>(u_host) + (size_t)k * bytes;
+    const char* fh = static_cast<const char*>(f_host) + (size_t)k * in_bytes;
+    char* uh = static_cast<char*>(u_host) + (size_t)k * out_bytes;
     if (k >= 2) ILS_TRY(cudaStreamWaitEvent(h2d, ev_comp[sl], 0));  // f slot consumed by batch k-2
-    ILS_TRY(cudaMemcpyAsync(fslot[sl], fh, bytes, cudaMemcpyHostToDevice, h2d));
+    ILS_TRY(cudaMemcpyAsync(fslot[sl], fh, in_bytes, cudaMemcpyHostToDevice, h2d));
     ILS_TRY(cudaEventRecord(ev_in[sl], h2d));
     ILS_TRY(cudaStreamWaitEvent(s, ev_in[sl], 0));
     if (k >= 2) ILS_TRY(cudaStreamWaitEvent(s, ev_out[sl], 0));  // u slot drained by batch k-2
-    ils_status r = ils_smooth(p, fslot[sl], uslot[sl], ps, ws, stream, st[sl], nullptr);
+    ils_status r = run(fslot[sl], uslot[sl], st[sl]);
     if (r != ILS_OK) {
       cleanup();
       return r;
     }
     ILS_TRY(cudaEventRecord(ev_comp[sl], s));
     ILS_TRY(cudaStreamWaitEvent(d2h, ev_comp[sl], 0));
-    ILS_TRY(cudaMemcpyAsync(uh, uslot[sl], bytes, cudaMemcpyDeviceToHost, d2h));
+    ILS_TRY(cudaMemcpyAsync(uh, uslot[sl], out_bytes, cudaMemcpyDeviceToHost, d2h));
     ILS_TRY(cudaMemcpyAsync(hstat + k, st[sl], sizeof(int32_t), cudaMemcpyDeviceToHost, d2h));
     ILS_TRY(cudaEventRecord(ev_out[sl], d2h));
   }
@@ -924,6 +957,34 @@ ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, 
     return fail(ILS_ENONFINITE, "non-finite iterate at iteration %d", worst);
   }
   return ILS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, int64_t ps, int32_t nbatches,
+                           void* ws, void* io_dev, void* stream, int32_t* bad_iter) {
+  if (!p || !f_host || !u_host || !ws || !io_dev) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
+  if (ps != (int64_t)p->H * p->W) return fail(ILS_EINVAL, "host planes must be dense (plane_stride == H*W)");
+  const size_t bytes = (size_t)p->B * ps * (p->dtype == ILS_F32 ? 4 : 8);
+  return host_pipeline(f_host, u_host, bytes, bytes, nbatches, io_dev, stream, bad_iter,
+                       [&](void* fd, void* ud, int32_t* st) { return ils_smooth(p, fd, ud, ps, ws, stream, st, nullptr); });
+}
+
+ils_status ils_smooth_host_u8(const ils_plan* p, const uint8_t* f_host, uint8_t* u_host, int32_t channels,
+                              int32_t nbatches, void* ws, void* io_dev, void* stream, int32_t* bad_iter) {
+  if (!p || !f_host || !u_host || !ws || !io_dev) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
+  const size_t bytes = (size_t)p->B * p->H * p->W;
+  return host_pipeline(f_host, u_host, bytes, bytes, nbatches, io_dev, stream, bad_iter,
+                       [&](void* fd, void* ud, int32_t* st) {
+                         return ils_smooth_u8(p, static_cast<const uint8_t*>(fd), static_cast<uint8_t*>(ud), channels,
+                                              ws, stream, st);
+                       });
 }
 
 ils_status ils_launch_pass(const ils_plan* p, int32_t pass, const void* f, void* u, int64_t ps, void* ws,

@@ -92,6 +92,15 @@ struct RowArgs {
   double* epart;     // energy partials [B][gridDim.x] or nullptr
   FftDev<T> fft;     // row transform (length N = W/2 packed, W otherwise)
   const cx<T>* wreal;  // exp(-2 pi i k / W), k = 0..N/2 (packed only)
+  // 8-bit interleaved frames (kernels specialised with SMODE >= kU8Modes):
+  // plane b is channel b % ch of frame b / ch in [frames][H][W][ch] bytes.
+  // F0 reads f8 (v / 255, formats.py read side) and writes the planar copy
+  // fcopy the later row passes add; FIN writes u8 = floor(clip01(u) 255 + 0.5)
+  // (formats.py:25-27).
+  const unsigned char* f8;
+  unsigned char* u8;
+  int ch;
+  T* fcopy;
 };
 
 template <typename T>
@@ -379,6 +388,22 @@ constexpr bool kBulkRows = sizeof(T) == 4 && FS::n > 0 && (2 * FS::n) % 8 == 0;
 template <class FS>
 constexpr int kRowBlocksOf = (FS::n > 0 && FS::ME <= 16) ? 3 : 2;
 
+// u8 value -> T exactly as the reference's v / 255.0 rounded to T
+// (correctly rounded division; equal to float(double(v) / 255) for all 256 v)
+__device__ __forceinline__ float u8_to(unsigned v, float) { return __fdiv_rn(float(v), 255.f); }
+__device__ __forceinline__ double u8_to(unsigned v, double) { return double(v) / 255.0; }
+// formats.py:25-27: floor(clip01(u) * 255 + 0.5) with the reference's two roundings
+__device__ __forceinline__ unsigned char quant8(float v) {
+  const float c = fminf(fmaxf(v, 0.f), 1.f);
+  return (unsigned char)floorf(__fadd_rn(__fmul_rn(c, 255.f), 0.5f));
+}
+__device__ __forceinline__ unsigned char quant8(double v) {
+  const double c = fmin(fmax(v, 0.0), 1.0);
+  return (unsigned char)floor(__dadd_rn(__dmul_rn(c, 255.0), 0.5));
+}
+
+constexpr int kU8Modes = 8;  // SMODE = kU8Modes + MODE_F0 / MODE_FIN: 8-bit frame ingest / egress
+
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -386,7 +411,10 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   __shared__ unsigned long long bars[kMaxBandLines];
   using Grp = GroupT<FS::G>;
   constexpr bool BULK = kBulkRows<T, FS> && PACKED;
-  const int MODE = SMODE >= 0 ? SMODE : A.mode;  // block-uniform
+  constexpr bool U8 = SMODE >= kU8Modes;
+  constexpr bool LOADF8 = U8 && SMODE - kU8Modes == MODE_F0;
+  constexpr bool BULKIN = BULK && !LOADF8;
+  const int MODE = U8 ? SMODE - kU8Modes : (SMODE >= 0 ? SMODE : A.mode);  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = FS::G > 0 ? FS::G : A.fft.G;
   const Grp g{tid / G, G, tid % G};
@@ -458,7 +486,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     // plans) or per-element cp.async (runtime plans), issued for every line
     // up front; each group then transforms its lines while later ones land.
     const int mine = (nl - g.id + ngroups - 1) / ngroups;  // lines owned by this group
-    if constexpr (BULK) {
+    if constexpr (BULKIN) {
       if (tid == 0) {
         for (int i = 0; i < nl; ++i) mbar_init(&bars[i], 1);
         mbar_fence_init();
@@ -484,7 +512,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         }
       }
       __syncthreads();
-    } else if (MODE != MODE_F0 || PACKED) {
+    } else if (!LOADF8 && (MODE != MODE_F0 || PACKED)) {
       for (int i = g.id; i < nl; i += ngroups) {
         const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
         cx<T>* z = L.line(i);
@@ -509,13 +537,24 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     for (int i = g.id; i < nl; i += ngroups, ++li) {
       const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
       cx<T>* z = L.line(i);
-      if constexpr (BULK) {
+      if constexpr (BULKIN) {
         mbar_wait(&bars[i], 0);
-      } else if (MODE != MODE_F0 || PACKED) {
+      } else if (!LOADF8 && (MODE != MODE_F0 || PACKED)) {
         cp_async_wait_keep(mine - 1 - li);
         g.sync();
       }
-      if (MODE == MODE_F0) {
+      if constexpr (LOADF8) {
+        // 8-bit ingest: channel ch of an interleaved row, plus the planar copy
+        // of the band's own rows for the later passes' f-add
+        const int C = A.ch;
+        const unsigned char* src = A.f8 + ((size_t)(b / C) * H * W + (size_t)y * W) * C + (b % C);
+        T* cp = (i >= 1 && i <= nb) ? A.fcopy + (size_t)b * A.f_ps + (size_t)(y0 + i) * A.f_rp : nullptr;
+        for (int x = g.rank; x < W; x += g.size()) {
+          const T v = u8_to(__ldg(src + (size_t)x * C), T{});
+          L.set(i, x, v);
+          if (cp) cp[x] = v;
+        }
+      } else if (MODE == MODE_F0) {
         if (!PACKED)
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
@@ -534,6 +573,23 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
 
     // ---------------- final pass: write u (and its energy)
     if (MODE == MODE_FIN) {
+      if constexpr (U8) {
+        // 8-bit egress: quantised, interleaved into channel ch of the frame
+        const int C = A.ch;
+        unsigned char* dst = A.u8 + (size_t)(b / C) * H * W * C + (b % C);
+        T chk = T(0);
+        for (int j = 0; j < nb; ++j) {
+          unsigned char* row = dst + (size_t)(r0 + j) * W * C;
+          for (int x = tid; x < W; x += nthr) {
+            const T v = L.get(j + off, x);
+            chk = fma_rn(v, T(0), chk);
+            row[(size_t)x * C] = quant8(v);
+          }
+        }
+        bad = !finite_(chk);
+        if (__syncthreads_or(bad) && tid == 0) atomicMin(A.status, A.iter);
+        return;
+      }
       double e = 0.0;
       T* upl = A.u + (size_t)b * A.u_ps;
       if (PACKED && !trace) {
@@ -902,6 +958,10 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
     if (a.mode == MODE_F0) k = k_row<T, PACKED, FS, WIDE, MODE_F0>;
     if (a.mode == MODE_IT) k = k_row<T, PACKED, FS, WIDE, MODE_IT>;
     if (a.mode == MODE_FIN) k = k_row<T, PACKED, FS, WIDE, MODE_FIN>;
+    if (a.mode == MODE_F0 && a.f8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_F0>;
+    if (a.mode == MODE_FIN && a.u8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_FIN>;
+  } else if (a.f8 || a.u8) {
+    return cudaErrorInvalidValue;  // no energy trace on the 8-bit path
   }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

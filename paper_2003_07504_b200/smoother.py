@@ -91,6 +91,39 @@ def smooth_batch(f, params: SmoothParams, trace: bool = False):
     return (u, energies) if trace else u
 
 
+def smooth_frames_u8(frames, params: SmoothParams, *, precision: str | None = None):
+    """8-bit frames through the fused ingest/egress path.
+
+    frames: uint8 [F, H, W, C], [H, W, C] or [H, W] (numpy or CUDA tensor;
+    C = 3 rgb or 1 gray, the PNG/PPM pixel layout of formats.py).  Returns
+    the same shape and kind: floor(clip01(u) * 255 + 0.5) of smooth_color on
+    the planes v / 255 (formats.py:25-27 + smoother.py:175-217), per channel.
+    """
+    if params.color_mode is ColorMode.LUMINANCE_ONLY:
+        raise ValueError("the 8-bit path smooths channels independently (PER_CHANNEL_RGB or gray)")
+    torch = rt._torch()
+    is_t = _is_tensor(frames)
+    t = frames if is_t else torch.from_numpy(np.ascontiguousarray(frames))
+    if t.dtype != torch.uint8:
+        raise ValueError(f"8-bit path expects uint8 frames, got {t.dtype}")
+    shape = tuple(t.shape)
+    if len(shape) == 2:
+        t4 = t.reshape(1, shape[0], shape[1], 1)
+    elif len(shape) == 3:
+        t4 = t.unsqueeze(0)
+    elif len(shape) == 4:
+        t4 = t
+    else:
+        raise ValueError(f"frames must be [H, W], [H, W, C] or [F, H, W, C], got {shape}")
+    if t4.shape[-1] not in (1, 3):
+        raise ValueError(f"expected 1 or 3 channels, got {t4.shape[-1]}")
+    if t4.numel() == 0:
+        raise ValueError("image plane must be non-empty")
+    u = rt.smooth_device_u8(t4.to("cuda") if not t4.is_cuda else t4, params.c_params(), precision)
+    u = u.reshape(shape)
+    return u if (is_t and frames.is_cuda) else u.cpu().numpy()
+
+
 def _check_plan(plan: SolverPlan, shape, params: SmoothParams):
     """smoother.py:149-159."""
     if (plan.height, plan.width) != tuple(shape):

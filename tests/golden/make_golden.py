@@ -106,6 +106,32 @@ def main():
         g[name + "_u"] = u
         g[name + "_prm"] = np.array([lam, -1.0 if beta0 is None else beta0, kappa, iters])
 
+    # --- 8-bit round trip through the reference's own codec path (formats.py read/quantize/write)
+    import tempfile
+
+    from ilsmooth import formats as F
+
+    for name, shape, params in (
+        ("u8_rgb", (24, 20, 3), ref.SmoothParams(ref.Charbonnier(0.8, 1e-4), 1.0)),
+        ("u8_gray", (30, 18), ref.SmoothParams(ref.Welsch(10 / 255), 30.0, iters=10, c=2.0)),
+    ):
+        arr = np.random.default_rng(31).integers(0, 256, size=shape, dtype=np.uint8)
+        with tempfile.TemporaryDirectory() as d:
+            src, dst = os.path.join(d, "in.ppm" if len(shape) == 3 else "in.png"), os.path.join(d, "out.png")
+            if len(shape) == 3:
+                F.write_image(src, ref.MultiImage.from_array(arr / 255.0))
+            else:
+                F.write_image(src, ref.MultiImage((arr / 255.0,), ref.GRAY))
+            img = F.read_image(src)
+            assert np.array_equal(np.rint(img.to_array() * 255).astype(np.uint8), arr)
+            F.write_image(dst, ref.smooth_color(img, params))
+            from PIL import Image
+
+            with Image.open(dst) as im:
+                out = np.asarray(im).copy()
+        g[name + "_in"] = arr
+        g[name + "_out"] = out
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 

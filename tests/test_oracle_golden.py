@@ -134,3 +134,11 @@ def test_hqs_field_step_is_grid_optimal():
         x, beta, lam = rng.uniform(-2, 2), rng.uniform(0.1, 5.0), rng.uniform(0.05, 2.0)
         m = float(O.soft_threshold(x, lam / (2 * beta)))
         assert beta * (x - m) ** 2 + lam * abs(m) <= float((beta * (x - grid) ** 2 + lam * np.abs(grid)).min()) + 1e-7
+
+
+def test_u8_round_trip_matches_reference_codec_path(g):
+    # formats.py:25-27,43 through the reference's own PNG/PPM writer and reader (make_golden.py)
+    a = O.smooth_u8(g["u8_rgb_in"], O.Charbonnier(0.8, 1e-4), 1.0)
+    assert np.array_equal(a, g["u8_rgb_out"])
+    b = O.smooth_u8(g["u8_gray_in"], O.Welsch(10 / 255), 30.0, 10, 2.0)
+    assert np.array_equal(b, g["u8_gray_out"])
