@@ -13,9 +13,12 @@ the iterations, by design.  Frames shard across ranks with no communication
 
 value     device throughput: frames/s over all ranks, inputs resident in HBM,
           one CUDA-graph replay per step, CUDA events, max over ranks.
-e2e       the same through the C ABI with HOST buffers (ils_smooth_host):
-          pinned host -> device copies, kernels, device -> host copies and the
+e2e       the same through the C ABI with HOST buffers (ils_smooth_host_u8):
+          pinned host 8-bit RGB frames (the reference's PNG/PPM pixel format)
+          -> device copies, kernels (v/255 ingest and the quantising store
+          fused into the first/last passes), device -> host copies and the
           status readback inside the timed region, pipelined over frames.
+          e2e_f32_planes: the same with fp32 planes (ils_smooth_host).
 roofline  the dominant kernel (fused row pass, iterations >= 1) timed alone
           with CUDA events on its stream: algorithmic bytes / time vs the
           measured HBM copy bandwidth in MEASURED_PEAKS.json.
@@ -356,10 +359,17 @@ def main():
     col_gbs = col_bytes / (ms_col / 1e3) / 1e9
 
     # ---- end to end through the C ABI with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        fh = torch.empty((F * CH, H, W), dtype=torch.float32, pin_memory=True)
-        fh.copy_(f.cpu())
+    def e2e_leg(u8):
+        """ils_smooth_host(_u8): pinned host frames in, results out, copies in the timed region."""
+        if u8:
+            gen8 = torch.Generator(device=dev)
+            gen8.manual_seed(20240607 + rank)
+            fd8 = torch.randint(0, 256, (F, H, W, CH), generator=gen8, device=dev, dtype=torch.uint8)
+            fh = torch.empty((F, H, W, CH), dtype=torch.uint8, pin_memory=True)
+            fh.copy_(fd8.cpu())
+        else:
+            fh = torch.empty((F * CH, H, W), dtype=torch.float32, pin_memory=True)
+            fh.copy_(f.cpu())
         uh = torch.empty_like(fh, pin_memory=True)
         io = C.c_size_t()
         _lib.check(L.ils_host_io_size(plan.ptr, C.byref(io)), "ils_host_io_size")
@@ -367,9 +377,14 @@ def main():
         bad = C.c_int32()
 
         def host_call():
-            _lib.check(L.ils_smooth_host(plan.ptr, C.c_void_p(fh.data_ptr()), C.c_void_p(uh.data_ptr()), ps, F // G,
-                                         C.c_void_p(ws.data_ptr()), C.c_void_p(iobuf.data_ptr()),
-                                         C.c_void_p(stream.cuda_stream), C.byref(bad)), "ils_smooth_host")
+            if u8:
+                _lib.check(L.ils_smooth_host_u8(plan.ptr, C.c_void_p(fh.data_ptr()), C.c_void_p(uh.data_ptr()), CH,
+                                                F // G, C.c_void_p(ws.data_ptr()), C.c_void_p(iobuf.data_ptr()),
+                                                C.c_void_p(stream.cuda_stream), C.byref(bad)), "ils_smooth_host_u8")
+            else:
+                _lib.check(L.ils_smooth_host(plan.ptr, C.c_void_p(fh.data_ptr()), C.c_void_p(uh.data_ptr()), ps,
+                                             F // G, C.c_void_p(ws.data_ptr()), C.c_void_p(iobuf.data_ptr()),
+                                             C.c_void_p(stream.cuda_stream), C.byref(bad)), "ils_smooth_host")
 
         for _ in range(max(1, args.warmup)):
             host_call()
@@ -382,10 +397,23 @@ def main():
         b.record(stream)
         barrier()
         ms_e2e = max_over_ranks(a.elapsed_time(b) / e2e_steps)
-        assert torch.equal(uh[:CH].to(dev), u[:CH]), "e2e output differs from device path"
-        e2e = {"value": round(world * F / (ms_e2e / 1e3), 2), "unit": "frames/s",
-               "h2d_bytes_per_step": F * CH * H * W * 4, "d2h_bytes_per_step": F * CH * H * W * 4 + (F // G) * 4,
-               "ms_per_step": round(ms_e2e, 3), "api": "ils_smooth_host (C ABI), pinned host fp32 planes"}
+        if u8:  # the fused 8-bit path equals the device path on the same frames
+            got = ils.smooth_frames_u8(fd8[:G], params)
+            assert torch.equal(uh[:G].to(dev), got), "e2e output differs from device path"
+            nbytes = F * CH * H * W
+            api = "ils_smooth_host_u8 (C ABI): pinned host 8-bit RGB frames in and out (the reference's PNG/PPM pixel path)"
+        else:
+            assert torch.equal(uh[:CH].to(dev), u[:CH]), "e2e output differs from device path"
+            nbytes = F * CH * H * W * 4
+            api = "ils_smooth_host (C ABI): pinned host fp32 planes in and out"
+        return {"value": round(world * F / (ms_e2e / 1e3), 2), "unit": "frames/s",
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + (F // G) * 4,
+                "ms_per_step": round(ms_e2e, 3), "api": api}
+
+    e2e = e2e_f32 = None
+    if not args.no_e2e:
+        e2e = e2e_leg(u8=True)
+        e2e_f32 = e2e_leg(u8=False)
 
     # ---- comparison: the same loop on cuFFT + torch elementwise, same frames
     cufft = None
@@ -433,6 +461,7 @@ def main():
                        "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec",
                                                           "col_cols", "col_group", "col_radix", "col_spec")}},
             "e2e": e2e,
+            "e2e_f32_planes": e2e_f32,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": round(row_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(row_gbs / peak, 4), "traffic": measured_traffic("k_row_it"),

@@ -102,11 +102,12 @@ ILS_API ils_status ils_smooth(const ils_plan* plan, const void* f_dev, void* u_d
 /* Same, with HOST buffers: `nbatches` consecutive batches of plan.batch
  * planes (plane_stride elements apart) are copied in, smoothed and copied
  * out, pipelined so batch k+1's host->device copy and batch k-1's
- * device->host copy overlap batch k's kernels (two I/O slots, three
- * streams).  Blocks until done, then decodes the status words: returns
+ * device->host copy overlap batch k's kernels, and consecutive batches run
+ * on two compute lanes (the caller's stream + workspace, and an internal
+ * stream whose workspace lives in io_dev).  Blocks until done, then decodes the status words: returns
  * ILS_ENONFINITE_INPUT / ILS_ENONFINITE with *bad_iter = first bad iteration
  * (-1 when clean).  workspace: ils_workspace_size bytes; io_dev:
- * ils_host_io_size bytes of device memory.  Host buffers should be pinned
+ * ils_host_io_size bytes of device memory (I/O slots + second workspace).  Host buffers should be pinned
  * (cudaHostAlloc) for the copies to overlap. */
 ILS_API ils_status ils_host_io_size(const ils_plan* plan, size_t* bytes);
 ILS_API ils_status ils_smooth_host(const ils_plan* plan, const void* f_host, void* u_host, int64_t plane_stride,

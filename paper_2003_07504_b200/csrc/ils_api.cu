@@ -863,11 +863,16 @@ ils_status ils_solve_ls(const ils_plan* p, const void* f, const void* mx, const 
                          static_cast<const double*>(my), static_cast<double*>(u), ps, ws, s, status);
 }
 
+constexpr int kIoSlots = 4;  // host pipeline: batches in flight (2 per compute lane)
+
 ils_status ils_host_io_size(const ils_plan* p, size_t* bytes) {
   if (!p || !bytes) return fail(ILS_EINVAL, "NULL argument");
   const size_t es = p->dtype == ILS_F32 ? 4 : 8;
   const size_t batch_bytes = ((size_t)p->B * p->H * p->W * es + 255) & ~size_t(255);
-  *bytes = 4 * batch_bytes + 256;  // 2 slots x (f, u) + 2 status words
+  size_t ws = 0;
+  ils_workspace_size(p, &ws);
+  // kIoSlots x (f, u) + status words + the second compute lane's workspace
+  *bytes = 2 * kIoSlots * batch_bytes + 1024 + ws;
   return ILS_OK;
 }
 
@@ -875,33 +880,47 @@ ils_status ils_host_io_size(const ils_plan* p, size_t* bytes) {
 
 namespace {
 
-// Pipelined host path shared by ils_smooth_host / ils_smooth_host_u8: batch k's
-// host->device copy and batch k-1's device->host copy overlap batch k's
-// kernels (two I/O slots, three streams).  run(f_dev, u_dev, status_dev)
-// enqueues one batch on the caller's stream.
+// Pipelined host path shared by ils_smooth_host / ils_smooth_host_u8: batch k
+// runs on compute lane k & 1 (the caller's stream with the caller's
+// workspace, or an internal stream with the second workspace carved from
+// io_dev), so consecutive batches' kernels overlap each other and the
+// host->device / device->host copies (kIoSlots I/O slots, so a lane's next
+// batch never waits for its previous result's device->host copy).
+// run(f_dev, u_dev, status_dev, ws, stream) enqueues one batch.
 template <class Run>
-ils_status host_pipeline(const void* f_host, void* u_host, size_t in_bytes, size_t out_bytes, int32_t nbatches,
-                         void* io_dev, void* stream, int32_t* bad_iter, Run run) {
+ils_status host_pipeline(const ils_plan* p, const void* f_host, void* u_host, size_t in_bytes, size_t out_bytes,
+                         int32_t nbatches, void* ws, void* io_dev, void* stream, int32_t* bad_iter, Run run) {
   if (bad_iter) *bad_iter = -1;
   const size_t slot_in = (in_bytes + 255) & ~size_t(255), slot_out = (out_bytes + 255) & ~size_t(255);
   char* io = static_cast<char*>(io_dev);
-  char* fslot[2] = {io, io + slot_in};
-  char* uslot[2] = {io + 2 * slot_in, io + 2 * slot_in + slot_out};
-  char* stw = io + 2 * slot_in + 2 * slot_out;
-  int32_t* st[2] = {reinterpret_cast<int32_t*>(stw), reinterpret_cast<int32_t*>(stw + 128)};
+  constexpr int NS = kIoSlots;
+  char* fslot[NS];
+  char* uslot[NS];
+  int32_t* st[NS];
+  for (int i = 0; i < NS; ++i) {
+    fslot[i] = io + i * slot_in;
+    uslot[i] = io + NS * slot_in + i * slot_out;
+    st[i] = reinterpret_cast<int32_t*>(io + NS * (slot_in + slot_out) + 128 * i);
+  }
+  // the I/O slots are sized for the plan's dtype; the second workspace follows them
+  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
+  const size_t full_slot = ((size_t)p->B * p->H * p->W * es + 255) & ~size_t(255);
+  void* wsl[2] = {ws, io + 2 * NS * full_slot + 1024};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t lane[2] = {s, nullptr};
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  cudaEvent_t ev_in[NS] = {}, ev_comp[NS] = {}, ev_out[NS] = {};
   int32_t* hstat = nullptr;
   ils_status rc = ILS_OK;
   auto cleanup = [&]() {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       if (ev_in[i]) cudaEventDestroy(ev_in[i]);
       if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
       if (ev_out[i]) cudaEventDestroy(ev_out[i]);
     }
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
+    if (lane[1]) cudaStreamDestroy(lane[1]);
     if (hstat) cudaFreeHost(hstat);
   };
 #define ILS_TRY(call)                                                                    \
@@ -915,7 +934,8 @@ ils_status host_pipeline(const void* f_host, void* u_host, size_t in_bytes, size
   } while (0)
   ILS_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
   ILS_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
+  ILS_TRY(cudaStreamCreateWithFlags(&lane[1], cudaStreamNonBlocking));
+  for (int i = 0; i < NS; ++i) {
     ILS_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
     ILS_TRY(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
     ILS_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
@@ -925,27 +945,29 @@ ils_status host_pipeline(const void* f_host, void* u_host, size_t in_bytes, size
   ILS_TRY(cudaEventRecord(ev_out[0], s));
   ILS_TRY(cudaStreamWaitEvent(h2d, ev_out[0], 0));
   ILS_TRY(cudaStreamWaitEvent(d2h, ev_out[0], 0));
+  ILS_TRY(cudaStreamWaitEvent(lane[1], ev_out[0], 0));
   for (int k = 0; k < nbatches; ++k) {
-    const int sl = k & 1;
+    const int sl = k % NS, ln = k & 1;
     const char* fh = static_cast<const char*>(f_host) + (size_t)k * in_bytes;
     char* uh = static_cast<char*>(u_host) + (size_t)k * out_bytes;
-    if (k >= 2) ILS_TRY(cudaStreamWaitEvent(h2d, ev_comp[sl], 0));  // f slot consumed by batch k-2
+    if (k >= NS) ILS_TRY(cudaStreamWaitEvent(h2d, ev_comp[sl], 0));  // f slot consumed by batch k-NS
     ILS_TRY(cudaMemcpyAsync(fslot[sl], fh, in_bytes, cudaMemcpyHostToDevice, h2d));
     ILS_TRY(cudaEventRecord(ev_in[sl], h2d));
-    ILS_TRY(cudaStreamWaitEvent(s, ev_in[sl], 0));
-    if (k >= 2) ILS_TRY(cudaStreamWaitEvent(s, ev_out[sl], 0));  // u slot drained by batch k-2
-    ils_status r = run(fslot[sl], uslot[sl], st[sl]);
+    ILS_TRY(cudaStreamWaitEvent(lane[ln], ev_in[sl], 0));
+    if (k >= NS) ILS_TRY(cudaStreamWaitEvent(lane[ln], ev_out[sl], 0));  // u slot drained by batch k-NS
+    ils_status r = run(fslot[sl], uslot[sl], st[sl], wsl[ln], lane[ln]);
     if (r != ILS_OK) {
       cleanup();
       return r;
     }
-    ILS_TRY(cudaEventRecord(ev_comp[sl], s));
+    ILS_TRY(cudaEventRecord(ev_comp[sl], lane[ln]));
     ILS_TRY(cudaStreamWaitEvent(d2h, ev_comp[sl], 0));
     ILS_TRY(cudaMemcpyAsync(uh, uslot[sl], out_bytes, cudaMemcpyDeviceToHost, d2h));
     ILS_TRY(cudaMemcpyAsync(hstat + k, st[sl], sizeof(int32_t), cudaMemcpyDeviceToHost, d2h));
     ILS_TRY(cudaEventRecord(ev_out[sl], d2h));
   }
   ILS_TRY(cudaStreamSynchronize(d2h));
+  ILS_TRY(cudaStreamSynchronize(lane[1]));
   ILS_TRY(cudaStreamSynchronize(s));
 #undef ILS_TRY
   int worst = ILS_STATUS_CLEAN;
@@ -970,8 +992,10 @@ ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, 
   if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
   if (ps != (int64_t)p->H * p->W) return fail(ILS_EINVAL, "host planes must be dense (plane_stride == H*W)");
   const size_t bytes = (size_t)p->B * ps * (p->dtype == ILS_F32 ? 4 : 8);
-  return host_pipeline(f_host, u_host, bytes, bytes, nbatches, io_dev, stream, bad_iter,
-                       [&](void* fd, void* ud, int32_t* st) { return ils_smooth(p, fd, ud, ps, ws, stream, st, nullptr); });
+  return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter,
+                       [&](void* fd, void* ud, int32_t* st, void* w, cudaStream_t ls) {
+                         return ils_smooth(p, fd, ud, ps, w, ls, st, nullptr);
+                       });
 }
 
 ils_status ils_smooth_host_u8(const ils_plan* p, const uint8_t* f_host, uint8_t* u_host, int32_t channels,
@@ -980,10 +1004,10 @@ ils_status ils_smooth_host_u8(const ils_plan* p, const uint8_t* f_host, uint8_t*
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
   const size_t bytes = (size_t)p->B * p->H * p->W;
-  return host_pipeline(f_host, u_host, bytes, bytes, nbatches, io_dev, stream, bad_iter,
-                       [&](void* fd, void* ud, int32_t* st) {
+  return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter,
+                       [&](void* fd, void* ud, int32_t* st, void* w, cudaStream_t ls) {
                          return ils_smooth_u8(p, static_cast<const uint8_t*>(fd), static_cast<uint8_t*>(ud), channels,
-                                              ws, stream, st);
+                                              w, ls, st);
                        });
 }
 

@@ -549,10 +549,37 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         const int C = A.ch;
         const unsigned char* src = A.f8 + ((size_t)(b / C) * H * W + (size_t)y * W) * C + (b % C);
         T* cp = (i >= 1 && i <= nb) ? A.fcopy + (size_t)b * A.f_ps + (size_t)(y0 + i) * A.f_rp : nullptr;
-        for (int x = g.rank; x < W; x += g.size()) {
-          const T v = u8_to(__ldg(src + (size_t)x * C), T{});
-          L.set(i, x, v);
-          if (cp) cp[x] = v;
+        if (C == 3 && (W & 3) == 0) {
+          // 4 pixels = 12 bytes = 3 aligned words per thread and step
+          // (rows start at multiples of 12 W bytes from the 256-aligned base)
+          const unsigned* w3 = reinterpret_cast<const unsigned*>(src - (b % C));
+          const int sh = b % C;
+#pragma unroll 4
+          for (int q = g.rank; q < W / 4; q += g.size()) {
+            const unsigned w[3] = {__ldg(w3 + 3 * q), __ldg(w3 + 3 * q + 1), __ldg(w3 + 3 * q + 2)};
+            T v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int pos = 3 * k + sh;  // byte of pixel k, channel sh
+              const unsigned wd = pos < 4 ? w[0] : (pos < 8 ? w[1] : w[2]);
+              v[k] = u8_to((wd >> (8 * (pos & 3))) & 0xffu, T{});
+              L.set(i, 4 * q + k, v[k]);
+            }
+            if (cp) {
+              if constexpr (sizeof(T) == 4) {
+                *reinterpret_cast<float4*>(cp + 4 * q) = make_float4(v[0], v[1], v[2], v[3]);
+              } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cp[4 * q + k] = v[k];
+              }
+            }
+          }
+        } else {
+          for (int x = g.rank; x < W; x += g.size()) {
+            const T v = u8_to(__ldg(src + (size_t)x * C), T{});
+            L.set(i, x, v);
+            if (cp) cp[x] = v;
+          }
         }
       } else if (MODE == MODE_F0) {
         if (!PACKED)
