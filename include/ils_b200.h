@@ -113,6 +113,23 @@ ILS_API ils_status ils_host_io_size(const ils_plan* plan, size_t* bytes);
 ILS_API ils_status ils_smooth_host(const ils_plan* plan, const void* f_host, void* u_host, int64_t plane_stride,
                                    int32_t nbatches, void* workspace, void* io_dev, void* stream, int32_t* bad_iter);
 
+/* Applications (applications.py).  ils_smooth_epilogue = ils_smooth whose
+ * final pass writes clip01(u + k (f - u)) instead of u (kind
+ * ILS_EPI_DETAIL): detail_enhance (:80-93) with k = DetailBoost.k, and the
+ * clip01 of clipart_clean / texture_smooth (:186-207) with k = 0. */
+typedef enum { ILS_EPI_NONE = 0, ILS_EPI_DETAIL = 1 } ils_epilogue_kind;
+typedef struct {
+  int32_t kind; /* ils_epilogue_kind */
+  double k;     /* boost, finite >= 0 (applications.py:29-31) */
+} ils_epilogue;
+ILS_API ils_status ils_smooth_epilogue(const ils_plan* plan, const void* f_dev, void* u_dev, int64_t plane_stride,
+                                       void* workspace, void* stream, int32_t* status_dev, const ils_epilogue* epi);
+/* gaussian_blur (applications.py:210-222) of `batch` planes: separable,
+ * radius ceil(3 sigma) <= 128, replicate edges, axis 0 then axis 1.
+ * tmp: batch * plane_stride elements of device scratch.  x may equal y. */
+ILS_API ils_status ils_gaussian_blur(const void* x, void* y, void* tmp, int32_t batch, int32_t height, int32_t width,
+                                     int64_t plane_stride, double sigma, int32_t dtype, void* stream);
+
 /* 8-bit interleaved frames, the reference's PNG/PPM pixel path fused into
  * the first and last passes (formats.py:25-27 read v/255, write
  * floor(clip01(u)*255 + 0.5); image.py MultiImage.from_array channel split).

@@ -202,6 +202,78 @@ def smooth_u8(arr, spec, lam, iters=4, c=None, workers=1):
                      for k in range(f.shape[-1])], axis=-1)
 
 
+# ---------------------------------------------------------------- applications
+def clip01(a):
+    """image.py:48-50."""
+    return np.clip(a, 0.0, 1.0)
+
+
+def detail_enhance(planes, spec, lam, k, iters=4, c=None):
+    """applications.py:80-93 (per channel)."""
+    if k == 1.0:
+        return [np.asarray(p) for p in planes]
+    out = []
+    for f in planes:
+        u = smooth_plane(f, spec, lam, iters, c)
+        out.append(clip01(u + k * (f - u)))
+    return out
+
+
+def gaussian_blur(plane, sigma):
+    """applications.py:210-222."""
+    from scipy.ndimage import convolve1d
+
+    plane = np.asarray(plane, dtype=np.float64)
+    if sigma == 0.0:
+        return np.array(plane)
+    radius = int(np.ceil(3.0 * sigma))
+    x = np.arange(-radius, radius + 1, dtype=np.float64)
+    kernel = np.exp(-(x * x) / (2.0 * sigma * sigma))
+    kernel /= kernel.sum()
+    out = convolve1d(plane, kernel, axis=0, mode="nearest")
+    return convolve1d(out, kernel, axis=1, mode="nearest")
+
+
+def clipart_clean(planes, gamma, lam):
+    """applications.py:186-197."""
+    return [clip01(smooth_plane(f, Welsch(gamma), lam, 10, 2.0)) for f in planes]
+
+
+def texture_smooth(planes, gamma, lam, sigma_pre=1.0):
+    """applications.py:200-207 (c defaults to Welsch's c0 = 2)."""
+    return [clip01(smooth_plane(gaussian_blur(f, sigma_pre), Welsch(gamma), lam, 15)) for f in planes]
+
+
+def _tonemap_finish(lum, rgb, log_lum_out, saturation):
+    lum_out = 10.0 ** log_lum_out  # applications.py:121-129
+    return [clip01((ch / lum) ** saturation * lum_out) for ch in rgb]
+
+
+def _compress_base(base, target_range):
+    spread = float(base.max() - base.min())  # applications.py:111-118
+    if spread < 1e-9:
+        raise ArithmeticError(f"degenerate base dynamic range {spread:g}")
+    return (base - base.max()) * (target_range / spread)
+
+
+def tonemap_single(lum, rgb, spec, lam, iters=4, c=None, target_range=2.0, saturation=0.6, log_offset=1e-6):
+    """applications.py:132-150."""
+    log_lum = np.log10(lum + log_offset)
+    base = smooth_plane(log_lum, spec, lam, iters, c)
+    out = _compress_base(base, target_range) + (log_lum - base)
+    return _tonemap_finish(lum, rgb, out, saturation)
+
+
+def tonemap_multi(lum, rgb, spec, lambdas, iters=4, c=None, target_range=2.0, saturation=0.6, log_offset=1e-6,
+                  weights=(1.0, 1.0, 1.0)):
+    """applications.py:153-183."""
+    log_lum = np.log10(lum + log_offset)
+    b = [smooth_plane(log_lum, spec, lm, iters, c) for lm in lambdas]
+    w0, w1, w2 = weights
+    out = _compress_base(b[2], target_range) + w2 * (b[1] - b[2]) + w1 * (b[0] - b[1]) + w0 * (log_lum - b[0])
+    return _tonemap_finish(lum, rgb, out, saturation)
+
+
 # ---------------------------------------------------------------- HQS baseline
 def soft_threshold(x, alpha):
     """penalty.py:168-177."""

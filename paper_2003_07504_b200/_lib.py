@@ -23,7 +23,7 @@ STATUS_CLEAN = 0x7F7F7F7F
 
 EXPORTS = (
     "ils_plan_create", "ils_hqs_plan_create", "ils_plan_destroy", "ils_workspace_size", "ils_smooth", "ils_smooth_host", "ils_smooth_u8",
-    "ils_smooth_host_u8",
+    "ils_smooth_host_u8", "ils_smooth_epilogue", "ils_gaussian_blur",
     "ils_host_io_size", "ils_launch_pass", "ils_slab_plan_create", "ils_slab_get_layout", "ils_slab_row_pass",
     "ils_slab_col_pass",
     "ils_solve_ls", "ils_rfft2", "ils_irfft2", "ils_rgb_yuv", "ils_plan_get_info", "ils_last_error",
@@ -38,6 +38,13 @@ class Params(C.Structure):
 
 class HqsParams(C.Structure):
     _fields_ = [("lam", C.c_double), ("beta0", C.c_double), ("kappa", C.c_double), ("iters", C.c_int32)]
+
+
+class Epilogue(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("k", C.c_double)]
+
+
+ILS_EPI_NONE, ILS_EPI_DETAIL = 0, 1
 
 
 class PlanInfo(C.Structure):
@@ -71,6 +78,9 @@ _SIGS = {
     "ils_smooth_host": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32)]),
     "ils_smooth_u8": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, _P]),
     "ils_smooth_host_u8": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32)]),
+    "ils_smooth_epilogue": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, _P, C.POINTER(Epilogue)]),
+    "ils_gaussian_blur": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_int32,
+                                    _P]),
     "ils_host_io_size": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
     "ils_launch_pass": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int64, _P, _P, _P]),
     "ils_solve_ls": (C.c_int, [_P, _P, _P, _P, _P, C.c_int64, _P, _P, _P]),

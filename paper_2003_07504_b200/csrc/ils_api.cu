@@ -538,7 +538,8 @@ cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
 // planar copy of f in the workspace for the later passes; FIN writes u8.
 template <typename T>
 ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, cudaStream_t s, int32_t* status,
-                    double* energies, const unsigned char* f8 = nullptr, unsigned char* u8 = nullptr, int ch = 1) {
+                    double* energies, const unsigned char* f8 = nullptr, unsigned char* u8 = nullptr, int ch = 1,
+                    const ils_epilogue* epi = nullptr) {
   cx<T>* Sa = static_cast<cx<T>*>(ws);
   cx<T>* Sb = reinterpret_cast<cx<T>*>(static_cast<char*>(ws) + p->spec_bytes);
   double* ep = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * p->spec_bytes + 256);
@@ -582,6 +583,11 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
   a.epart = energies ? ep + iters * per_pass : nullptr;
   a.u8 = u8;
   a.ch = ch;
+  if (epi && epi->kind == ILS_EPI_DETAIL) {
+    a.epi = 1;
+    a.epi_k = T(epi->k);
+    if (f8) a.f = a.fcopy;
+  }
   ILS_CUDA(launch_row<T>(p, MODE_FIN, a, s));
   if (energies) {
     for (int n = 0; n <= iters; ++n) {
@@ -834,6 +840,60 @@ ils_status ils_smooth(const ils_plan* p, const void* f, void* u, int64_t ps, voi
   if (p->dtype == ILS_F32)
     return smooth_t<float>(p, static_cast<const float*>(f), static_cast<float*>(u), ps, ws, s, status, energies);
   return smooth_t<double>(p, static_cast<const double*>(f), static_cast<double*>(u), ps, ws, s, status, energies);
+}
+
+ils_status ils_smooth_epilogue(const ils_plan* p, const void* f, void* u, int64_t ps, void* ws, void* stream,
+                              int32_t* status, const ils_epilogue* epi) {
+  if (!p || !f || !u || !ws || !status || !epi) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (p->slab) return fail(ILS_EINVAL, "slab plans run through ils_slab_row_pass / ils_slab_col_pass");
+  if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
+  if (epi->kind != ILS_EPI_NONE && epi->kind != ILS_EPI_DETAIL) return fail(ILS_EINVAL, "unknown epilogue %d", epi->kind);
+  if (!(epi->k >= 0.0 && std::isfinite(epi->k)))  // DetailBoost.__post_init__ (applications.py:29-31)
+    return fail(ILS_EINVAL, "boost k must be finite and >= 0, got %g", epi->k);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->dtype == ILS_F32)
+    return smooth_t<float>(p, static_cast<const float*>(f), static_cast<float*>(u), ps, ws, s, status, nullptr,
+                           nullptr, nullptr, 1, epi);
+  return smooth_t<double>(p, static_cast<const double*>(f), static_cast<double*>(u), ps, ws, s, status, nullptr,
+                          nullptr, nullptr, 1, epi);
+}
+
+ils_status ils_gaussian_blur(const void* x, void* y, void* tmp, int32_t batch, int32_t height, int32_t width,
+                             int64_t ps, double sigma, int32_t dtype, void* stream) {
+  if (!x || !y || !tmp) return fail(ILS_EINVAL, "NULL argument");
+  if (batch < 1 || height < 1 || width < 1 || ps < (int64_t)height * width) return fail(ILS_EINVAL, "bad blur shape");
+  if (dtype != ILS_F32 && dtype != ILS_F64) return fail(ILS_EINVAL, "unknown dtype %d", dtype);
+  if (!(sigma >= 0.0 && std::isfinite(sigma))) return fail(ILS_EINVAL, "sigma must be finite and >= 0, got %g", sigma);
+  const int r = sigma == 0.0 ? 0 : (int)std::ceil(3.0 * sigma);
+  if (r > kMaxGaussRadius) return fail(ILS_EUNSUPPORTED, "sigma %g: blur radius %d > %d", sigma, r, kMaxGaussRadius);
+  // kernel = exp(-x^2 / 2 sigma^2) / sum (applications.py:217-220), in double
+  std::vector<double> w(r + 1, 1.0);
+  double sum = 1.0;
+  for (int j = 1; j <= r; ++j) {
+    w[j] = std::exp(-(double)j * j / (2.0 * sigma * sigma));
+    sum += 2.0 * w[j];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto run = [&](auto tag) -> ils_status {
+    using T = decltype(tag);
+    GaussW<T> g{};
+    g.r = r;
+    // numpy normalises the full (2r+1)-tap array: kernel /= kernel.sum(), summed left to right
+    double tot = 0.0;
+    for (int j = -r; j <= r; ++j) tot += w[std::abs(j)];
+    (void)sum;
+    for (int j = 0; j <= r; ++j) g.w[j] = T(w[j] / tot);
+    const dim3 gc((width + 127) / 128, (height + 31) / 32, batch);
+    k_gauss_cols<T><<<gc, 128, 0, s>>>(static_cast<const T*>(x), static_cast<T*>(tmp), height, width, ps, g);
+    ILS_CUDA(cudaGetLastError());
+    const size_t sm = (size_t)(width + 2 * r) * sizeof(T);
+    if (sm > 48 * 1024) ILS_CUDA(cudaFuncSetAttribute(k_gauss_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_gauss_rows<T><<<dim3(height, batch), 256, sm, s>>>(static_cast<const T*>(tmp), static_cast<T*>(y), width, ps, g);
+    ILS_CUDA(cudaGetLastError());
+    return ILS_OK;
+  };
+  return dtype == ILS_F32 ? run(float{}) : run(double{});
 }
 
 ils_status ils_smooth_u8(const ils_plan* p, const uint8_t* f, uint8_t* u, int32_t channels, void* ws, void* stream,

@@ -101,6 +101,10 @@ struct RowArgs {
   unsigned char* u8;
   int ch;
   T* fcopy;
+  // FIN epilogue (applications.py): epi = 1 writes clip01(u + k (f - u))
+  // (detail_enhance, :80-93; k = 0 is the clip01 of clipart/texture presets)
+  int epi;
+  T epi_k;
 };
 
 template <typename T>
@@ -402,6 +406,15 @@ __device__ __forceinline__ unsigned char quant8(double v) {
   return (unsigned char)floor(__dadd_rn(__dmul_rn(c, 255.0), 0.5));
 }
 
+// applications.py:80-93 / image.clip01: clip01(u + k (f - u)) with the
+// reference's roundings (no contraction); k = 0 is clip01(u).
+template <typename T>
+__device__ __forceinline__ T detail_epilogue(T u, T f, T k) {
+  T v = u;
+  if (k != T(0)) v = v + mul_rn(k, f - u);
+  return fmin(fmax(v, T(0)), T(1));
+}
+
 constexpr int kU8Modes = 8;  // SMODE = kU8Modes + MODE_F0 / MODE_FIN: 8-bit frame ingest / egress
 
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
@@ -623,8 +636,12 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         // finiteness (smoother.py:166-167): fma(x, 0, c) is NaN iff some x is not finite
         T chk = T(0);
         for (int j = 0; j < nb; ++j) {
-          const T* z = reinterpret_cast<const T*>(L.line(j + off));
-          for (int x = tid; x < W; x += nthr) chk = fma_rn(z[x], T(0), chk);
+          T* z = reinterpret_cast<T*>(L.line(j + off));
+          const T* fr = fpl ? fpl + (size_t)(r0 + j) * A.f_rp : nullptr;
+          for (int x = tid; x < W; x += nthr) {
+            chk = fma_rn(z[x], T(0), chk);
+            if (A.epi) z[x] = detail_epilogue(z[x], A.epi_k != T(0) ? fr[x] : T(0), A.epi_k);
+          }
         }
         if constexpr (BULK) {
           __syncthreads();
@@ -633,6 +650,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
                           l2_evict_first());
         } else {
           const int np = W / 2;
+          if (A.epi) __syncthreads();  // pairs below span other threads' epilogue elements
           for (int j = 0; j < nb; ++j) {
             cx<T>* dst = reinterpret_cast<cx<T>*>(upl + (size_t)(r0 + j) * A.u_rp);
             const cx<T>* z = L.line(j + off);
@@ -648,7 +666,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         const int j = t / W, x = t - j * W;
         const T uc = L.get(j + off, x);
         bad |= !finite_(uc);
-        upl[(size_t)(r0 + j) * A.u_rp + x] = uc;
+        upl[(size_t)(r0 + j) * A.u_rp + x] =
+            A.epi ? detail_epilogue(uc, A.epi_k != T(0) ? fpl[(size_t)(r0 + j) * A.f_rp + x] : T(0), A.epi_k) : uc;
         if (trace) {
           const T gx = L.get(j + off, wrapi(x + 1, W)) - uc;
           const T gy = L.get(j + off + 1, x) - uc;
@@ -942,6 +961,51 @@ __global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long n
       q[plane_stride] = (a - T(0.299) * r - T(0.114) * bb) / T(0.587);
       q[2 * plane_stride] = bb;
     }
+  }
+}
+
+// ------------------------------------------------------------ applications
+// gaussian_blur (applications.py:210-222): separable, radius ceil(3 sigma),
+// replicate ("nearest") edges, axis 0 then axis 1.  Sums follow scipy's
+// symmetric correlate: w[r] x[i] + sum_j w[r+j] (x[i+j] + x[i-j]).
+constexpr int kMaxGaussRadius = 128;
+template <typename T>
+struct GaussW {
+  int r;
+  T w[kMaxGaussRadius + 1];  // w[j] = weight at offset j (symmetric)
+};
+
+template <typename T>
+__global__ void k_gauss_cols(const T* __restrict__ x, T* __restrict__ y, int H, int W, long long ps, GaussW<T> g) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.y * 32;
+  if (c >= W) return;
+  const T* xp = x + (size_t)blockIdx.z * ps;
+  T* yp = y + (size_t)blockIdx.z * ps;
+  for (int r = r0; r < min(r0 + 32, H); ++r) {
+    T acc = g.w[0] * xp[(size_t)r * W + c];
+    for (int j = 1; j <= g.r; ++j) {
+      const int a = min(r + j, H - 1), b = max(r - j, 0);
+      acc = acc + g.w[j] * (xp[(size_t)a * W + c] + xp[(size_t)b * W + c]);
+    }
+    yp[(size_t)r * W + c] = acc;
+  }
+}
+
+template <typename T>
+__global__ void k_gauss_rows(const T* __restrict__ x, T* __restrict__ y, int W, long long ps, GaussW<T> g) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  T* row = reinterpret_cast<T*>(gsm);  // [r halo][W][r halo], replicate edges
+  const int rr = blockIdx.x;
+  const T* xp = x + (size_t)blockIdx.y * ps + (size_t)rr * W;
+  T* yp = y + (size_t)blockIdx.y * ps + (size_t)rr * W;
+  for (int i = threadIdx.x; i < W + 2 * g.r; i += blockDim.x) row[i] = xp[min(max(i - g.r, 0), W - 1)];
+  __syncthreads();
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    const T* q = row + c + g.r;
+    T acc = g.w[0] * q[0];
+    for (int j = 1; j <= g.r; ++j) acc = acc + g.w[j] * (q[j] + q[-j]);
+    yp[c] = acc;
   }
 }
 

@@ -132,6 +132,28 @@ def main():
         g[name + "_in"] = arr
         g[name + "_out"] = out
 
+    # --- applications (applications.py:80-222), small inputs through the real presets
+    rng = np.random.default_rng(41)
+    img = ref.MultiImage.from_array(rng.random((18, 22, 3)))
+    g["app_img"] = img.to_array()
+    prm = ref.SmoothParams(ref.Charbonnier(0.8, 1e-4), 1.0)
+    g["app_detail3"] = ref.detail_enhance(img, prm, ref.DetailBoost(3.0)).to_array()
+    g["app_detail0"] = ref.detail_enhance(img, prm, ref.DetailBoost(0.0)).to_array()
+    g["app_clipart"] = ref.clipart_clean(img, 10 / 255, 20.0).to_array()
+    g["app_texture"] = ref.texture_smooth(img, 10 / 255, 30.0, sigma_pre=1.0).to_array()
+    g["app_blur15"] = ref.gaussian_blur(img.channels[0], 1.5)
+    g["app_blur07"] = ref.gaussian_blur(img.channels[1], 0.7)
+    lum = 10.0 ** rng.uniform(-2, 2, (24, 20))
+    tint = np.stack([np.full(lum.shape, 0.9), np.full(lum.shape, 0.7), np.full(lum.shape, 0.5)], -1)
+    rgb = ref.MultiImage.from_array(lum[..., None] * tint, ref.RGB)
+    y = ref.luminance(rgb)
+    g["app_hdr_rgb"] = rgb.to_array()
+    tp = ref.TonemapParams(ref.SmoothParams(ref.Charbonnier(1.0, 1e-4), 2.0), target_range=1.5)
+    g["app_tm_single"] = ref.tonemap_single(y, rgb, tp).to_array()
+    tpm = ref.TonemapParams(ref.SmoothParams(ref.Charbonnier(1.0, 1e-4), 5.0), lambdas=(0.125, 1.0, 8.0),
+                            weights=(1.2, 0.8, 1.0))
+    g["app_tm_multi"] = ref.tonemap_multi(y, rgb, tpm).to_array()
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 

@@ -21,7 +21,7 @@ def _header_symbols():
 def test_library_loads_and_exports_every_header_symbol():
     L = _lib.lib()
     syms = _header_symbols()
-    assert len(syms) == 21
+    assert len(syms) == 23
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
@@ -199,3 +199,21 @@ def test_hqs_params_validation_matches_reference():
     p = _lib.Params(_lib.ILS_SOFT, 0.0, 0.0, 0.0, 1.0, 1.0, 4)
     with pytest.raises(ValueError):
         _lib.check(L.ils_plan_create(C.byref(h), 1, 8, 8, C.byref(p), _lib.ILS_F32, -1), "create")
+
+
+def test_application_params_validation():
+    # applications.py:23-77 (host-side, before any work)
+    import paper_2003_07504_b200 as ils
+
+    with pytest.raises(ValueError):
+        ils.DetailBoost(-0.5)
+    with pytest.raises(ValueError):
+        ils.DetailBoost(float("inf"))
+    assert ils.DetailBoost().k == 3.0
+    base = ils.SmoothParams(ils.Charbonnier(1.0, 1e-4), 1.0)
+    for kw in (dict(target_range=0.0), dict(saturation=0.0), dict(saturation=1.2), dict(log_offset=0.0),
+               dict(lambdas=(1.0, 2.0)), dict(lambdas=(8.0, 1.0, 0.125)),
+               dict(lambdas=(0.125, 1.0, 8.0), weights=(1.0, 1.0))):
+        with pytest.raises(ValueError):
+            ils.TonemapParams(base, **kw)
+    ils.TonemapParams(base, lambdas=(1.0, 1.0, 1.0))

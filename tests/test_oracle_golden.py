@@ -142,3 +142,25 @@ def test_u8_round_trip_matches_reference_codec_path(g):
     assert np.array_equal(a, g["u8_rgb_out"])
     b = O.smooth_u8(g["u8_gray_in"], O.Welsch(10 / 255), 30.0, 10, 2.0)
     assert np.array_equal(b, g["u8_gray_out"])
+
+
+def test_applications_match_reference_goldens(g):
+    # applications.py:80-222 via tests/golden/make_golden.py
+    img = g["app_img"]
+    planes = [img[..., k] for k in range(3)]
+    st = lambda ps: np.stack(ps, -1)  # noqa: E731
+    cb = O.Charbonnier(0.8, 1e-4)
+    assert np.max(np.abs(st(O.detail_enhance(planes, cb, 1.0, 3.0)) - g["app_detail3"])) < 1e-12
+    assert np.max(np.abs(st(O.detail_enhance(planes, cb, 1.0, 0.0)) - g["app_detail0"])) < 1e-12
+    assert np.max(np.abs(st(O.clipart_clean(planes, 10 / 255, 20.0)) - g["app_clipart"])) < 1e-12
+    assert np.max(np.abs(st(O.texture_smooth(planes, 10 / 255, 30.0, 1.0)) - g["app_texture"])) < 1e-12
+    assert np.array_equal(O.gaussian_blur(planes[0], 1.5), g["app_blur15"])
+    assert np.array_equal(O.gaussian_blur(planes[1], 0.7), g["app_blur07"])
+    rgb = g["app_hdr_rgb"]
+    ch = [rgb[..., k] for k in range(3)]
+    y = 0.299 * ch[0] + 0.587 * ch[1] + 0.114 * ch[2]
+    c1 = O.Charbonnier(1.0, 1e-4)
+    got = st(O.tonemap_single(y, ch, c1, 2.0, target_range=1.5))
+    assert np.max(np.abs(got - g["app_tm_single"])) < 1e-12
+    got = st(O.tonemap_multi(y, ch, c1, (0.125, 1.0, 8.0), weights=(1.2, 0.8, 1.0)))
+    assert np.max(np.abs(got - g["app_tm_multi"])) < 1e-12
