@@ -154,12 +154,17 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 // mu = c x - phi'(x) (penalty.py:117-126) with phi' from penalty.py:64-66
 // (Charbonnier: p x (x^2+eps)^(p/2-1)) or 93-96 (Welsch: 2x exp(-x^2/2g^2)),
 // written as x * (c + coef * 2^(E * Lg)).
-template <typename T>
+// SOFT: kernels that may run the soft threshold (kind 2) apply the floor;
+// the specialised ILS kernels never see kind 2 (launch_row_impl routes HQS
+// plans to the generic kernel) and skip it.
+template <bool SOFT, typename T>
 __device__ __forceinline__ T aux(T x, const PenaltyDev<T>& P) {
   const T q = fma_rn(x, x, P.eps0);
   const T lg = P.kind != 1 ? lg2_(q) : q;
   const T t = ex2_(mul_rn(P.E, lg));
-  return mul_rn(x, fmax(fma_rn(P.coef, t, P.c), P.floor));
+  T v = fma_rn(P.coef, t, P.c);
+  if constexpr (SOFT) v = fmax(v, P.floor);
+  return mul_rn(x, v);
 }
 // phi(x): penalty.py:60-62, 88-91 (energy trace only)
 template <typename T>
@@ -415,7 +420,12 @@ __device__ __forceinline__ T detail_epilogue(T u, T f, T k) {
   return fmin(fmax(v, T(0)), T(1));
 }
 
-constexpr int kU8Modes = 8;  // SMODE = kU8Modes + MODE_F0 / MODE_FIN: 8-bit frame ingest / egress
+constexpr int kU8Modes = 8;
+// stencil rows per barrier (rhs of that many rows held in registers)
+#ifndef ILS_STENCIL_ROWS
+#define ILS_STENCIL_ROWS 3
+#endif
+constexpr int kStencilRows = ILS_STENCIL_ROWS;  // SMODE = kU8Modes + MODE_F0 / MODE_FIN: 8-bit frame ingest / egress
 
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
@@ -427,6 +437,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   constexpr bool U8 = SMODE >= kU8Modes;
   constexpr bool LOADF8 = U8 && SMODE - kU8Modes == MODE_F0;
   constexpr bool BULKIN = BULK && !LOADF8;
+  constexpr bool SOFTOK = SMODE < 0 || U8;  // kernels that accept the soft-threshold penalty
   const int MODE = U8 ? SMODE - kU8Modes : (SMODE >= 0 ? SMODE : A.mode);  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int G = FS::G > 0 ? FS::G : A.fft.G;
@@ -500,10 +511,12 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     // up front; each group then transforms its lines while later ones land.
     const int mine = (nl - g.id + ngroups - 1) / ngroups;  // lines owned by this group
     if constexpr (BULKIN) {
-      if (tid == 0) {
-        for (int i = 0; i < nl; ++i) mbar_init(&bars[i], 1);
+      // thread i arms line i's barrier and issues its copy (parallel issue)
+      if (tid < nl) {
+        mbar_init(&bars[tid], 1);
         mbar_fence_init();
-        for (int i = 0; i < nl; ++i) {
+        {
+          const int i = tid;
           const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
           if (MODE == MODE_F0) {
             const unsigned bytes = (unsigned)(W * sizeof(T));
@@ -706,83 +719,98 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
 #pragma unroll
           for (int q = 0; q < QW; ++q) {
             const int x = gg * QW + q;
-            myup[gi][q] = x < W ? aux(L.get(1, x) - L.get(0, x), P) : T(0);
+            myup[gi][q] = x < W ? aux<SOFTOK>(L.get(1, x) - L.get(0, x), P) : T(0);
             fcur[gi][q] = (TR && is_it && x < W) ? __ldg(fpl + (size_t)r0 * A.f_rp + x) : T(0);
           }
         }
       }
-      for (int j = 0; j < nb; ++j) {
-        const int i = j + 1;
-        T rhs[GMAX][QW];
-        T fnext[GMAX][QW];
+      // rows in blocks of KB: the rhs of a block stays in registers until one
+      // barrier shows every thread is past the block (a row reads its own
+      // line and the one below, so lines <= jb + KB are free to take rhs)
+      constexpr int KB = TR ? 1 : kStencilRows;
+      for (int jb = 0; jb < nb; jb += KB) {
+        T rhs[KB][GMAX][QW];
 #pragma unroll
-        for (int gi = 0; gi < GMAX; ++gi) {
-          const int gg = tid + gi * nthr;
-          if (gg < ng) {
-            const int x0 = gg * QW;
-            const bool full = PACKED && x0 + QW <= W;
-            if (TR && is_it) {
-              const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp + x0;
+        for (int kk = 0; kk < KB; ++kk) {
+          const int j = jb + kk;
+          if (j >= nb) break;  // block-uniform
+          const int i = j + 1;
+          T fnext[GMAX][QW];
 #pragma unroll
-              for (int q = 0; q < QW; ++q) fnext[gi][q] = (full || x0 + q < W) ? __ldg(fr + q) : T(0);
-            }
-            T uc[QW], ud[QW];
-            if (full) {
-              L.template get_strip<QW>(i, x0, uc);
-              L.template get_strip<QW>(i + 1, x0, ud);
-            } else {
+          for (int gi = 0; gi < GMAX; ++gi) {
+            const int gg = tid + gi * nthr;
+            if (gg < ng) {
+              const int x0 = gg * QW;
+              const bool full = PACKED && x0 + QW <= W;
+              if (TR && is_it) {
+                const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp + x0;
+#pragma unroll
+                for (int q = 0; q < QW; ++q) fnext[gi][q] = (full || x0 + q < W) ? __ldg(fr + q) : T(0);
+              }
+              T uc[QW], ud[QW];
+              if (full) {
+                L.template get_strip<QW>(i, x0, uc);
+                L.template get_strip<QW>(i + 1, x0, ud);
+              } else {
+#pragma unroll
+                for (int q = 0; q < QW; ++q) {
+                  const int x = x0 + q;
+                  uc[q] = x < W ? L.get(i, x) : T(0);
+                  ud[q] = x < W ? L.get(i + 1, x) : T(0);
+                }
+              }
+              T mxp = aux<SOFTOK>(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
+              const T uright = L.get(i, wrapi(full ? x0 + QW : min(x0 + QW, W), W));
 #pragma unroll
               for (int q = 0; q < QW; ++q) {
-                const int x = x0 + q;
-                uc[q] = x < W ? L.get(i, x) : T(0);
-                ud[q] = x < W ? L.get(i + 1, x) : T(0);
-              }
-            }
-            T mxp = aux(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
-            const T uright = L.get(i, wrapi(full ? x0 + QW : min(x0 + QW, W), W));
-#pragma unroll
-            for (int q = 0; q < QW; ++q) {
-              if (full || x0 + q < W) {
-                const T ur = (q + 1 < QW && (full || x0 + q + 1 < W)) ? uc[q + 1] : uright;
-                const T gx = ur - uc[q];
-                const T gy = ud[q] - uc[q];
-                const T mxq = aux(gx, P);
-                const T myq = aux(gy, P);
-                const T a = (mxp - mxq) + (myup[gi][q] - myq);
-                // iteration >= 1: rhs holds lam/2 D^T mu only; f is added as the
-                // r2c's first pass loads each element (phase C), off the
-                // stencil's critical path
-                const T fv = is_it ? fcur[gi][q] : uc[q];
-                rhs[gi][q] = is_it ? mul_rn(P.lam2, a) : fma_rn(P.lam2, a, fv);
-                chk = fma_rn(uc[q], T(0), chk);
-                if constexpr (TR) {
-                  const T d = uc[q] - fv;
-                  e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
+                if (full || x0 + q < W) {
+                  const T ur = (q + 1 < QW && (full || x0 + q + 1 < W)) ? uc[q + 1] : uright;
+                  const T gx = ur - uc[q];
+                  const T gy = ud[q] - uc[q];
+                  const T mxq = aux<SOFTOK>(gx, P);
+                  const T myq = aux<SOFTOK>(gy, P);
+                  const T a = (mxp - mxq) + (myup[gi][q] - myq);
+                  // iteration >= 1: rhs holds lam/2 D^T mu only; f is added as the
+                  // r2c's first pass loads each element (phase C), off the
+                  // stencil's critical path
+                  const T fv = is_it ? fcur[gi][q] : uc[q];
+                  rhs[kk][gi][q] = is_it ? mul_rn(P.lam2, a) : fma_rn(P.lam2, a, fv);
+                  chk = fma_rn(uc[q], T(0), chk);
+                  if constexpr (TR) {
+                    const T d = uc[q] - fv;
+                    e += double(d) * double(d) + double(P.lam) * (double(phi(gx, P)) + double(phi(gy, P)));
+                  }
+                  myup[gi][q] = myq;
+                  mxp = mxq;
+                } else {
+                  rhs[kk][gi][q] = T(0);
                 }
-                myup[gi][q] = myq;
-                mxp = mxq;
-              } else {
-                rhs[gi][q] = T(0);
+              }
+              if constexpr (TR) {
+#pragma unroll
+                for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
               }
             }
           }
         }
         __syncthreads();
 #pragma unroll
-        for (int gi = 0; gi < GMAX; ++gi) {
-          const int gg = tid + gi * nthr;
-          if (gg < ng) {
-            const int x0 = gg * QW;
-            if (PACKED && x0 + QW <= W) {
-              L.template set_strip<QW>(j, x0, rhs[gi]);
-            } else {
+        for (int kk = 0; kk < KB; ++kk) {
+          const int j = jb + kk;
+          if (j >= nb) break;
 #pragma unroll
-              for (int q = 0; q < QW; ++q)
-                if (x0 + q < W) L.set(j, x0 + q, rhs[gi][q]);
+          for (int gi = 0; gi < GMAX; ++gi) {
+            const int gg = tid + gi * nthr;
+            if (gg < ng) {
+              const int x0 = gg * QW;
+              if (PACKED && x0 + QW <= W) {
+                L.template set_strip<QW>(j, x0, rhs[kk][gi]);
+              } else {
+#pragma unroll
+                for (int q = 0; q < QW; ++q)
+                  if (x0 + q < W) L.set(j, x0 + q, rhs[kk][gi][q]);
+              }
             }
-#pragma unroll
-            if (TR)
-              for (int q = 0; q < QW; ++q) fcur[gi][q] = fnext[gi][q];
           }
         }
       }
@@ -1044,15 +1072,16 @@ cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t 
 #ifdef ILS_DEFINE_LAUNCHERS
 template <typename T, bool PACKED, class FS, bool WIDE>
 cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  // generic kernel (SMODE -1): energy trace, or the HQS soft threshold (kind 2)
   auto k = k_row<T, PACKED, FS, WIDE, -1>;
-  if (a.epart == nullptr) {
+  if (a.f8 || a.u8) {
+    if (a.epart) return cudaErrorInvalidValue;  // no energy trace on the 8-bit path
+    if (a.mode == MODE_F0 && a.f8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_F0>;
+    if (a.mode == MODE_FIN && a.u8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_FIN>;
+  } else if (a.epart == nullptr && (a.pen.kind != 2 || a.mode == MODE_FIN)) {
     if (a.mode == MODE_F0) k = k_row<T, PACKED, FS, WIDE, MODE_F0>;
     if (a.mode == MODE_IT) k = k_row<T, PACKED, FS, WIDE, MODE_IT>;
     if (a.mode == MODE_FIN) k = k_row<T, PACKED, FS, WIDE, MODE_FIN>;
-    if (a.mode == MODE_F0 && a.f8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_F0>;
-    if (a.mode == MODE_FIN && a.u8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_FIN>;
-  } else if (a.f8 || a.u8) {
-    return cudaErrorInvalidValue;  // no energy trace on the 8-bit path
   }
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
