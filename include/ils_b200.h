@@ -217,6 +217,9 @@ typedef struct {
   int32_t col_radix[16];
   int64_t spec_pitch;        /* complex elements per spectrum row */
   int32_t launches_per_call; /* kernels one ils_smooth launches (no trace) */
+  int32_t col2_spec;         /* two-stage column solve kernel id, -1 = k_col */
+  int32_t col2_n1, col2_n2;  /* its split H = n1 * n2 */
+  int32_t col2_cols;         /* spectrum columns per CTA */
 } ils_plan_info;
 ILS_API ils_status ils_plan_get_info(const ils_plan* plan, ils_plan_info* info);
 

@@ -54,7 +54,8 @@ class PlanInfo(C.Structure):
         "col_cols", "col_threads", "col_grid", "col_smem",
         "row_passes", "col_passes", "row_group", "col_group", "row_spec", "col_spec", "row_swz", "col_swz")] + [
         ("row_radix", C.c_int32 * 16), ("col_radix", C.c_int32 * 16),
-        ("spec_pitch", C.c_int64), ("launches_per_call", C.c_int32)]
+        ("spec_pitch", C.c_int64), ("launches_per_call", C.c_int32),
+        ("col2_spec", C.c_int32), ("col2_n1", C.c_int32), ("col2_n2", C.c_int32), ("col2_cols", C.c_int32)]
 
     def as_dict(self):
         d = {n: getattr(self, n) for n, _ in self._fields_ if n not in ("row_radix", "col_radix")}

@@ -24,9 +24,22 @@ UNITS = ([("ils_api.cu", "api", [])]
          + [("ils_inst.cu", f"row_rt_{t}", [f"-DILS_INST_ROW_RT={t}"]) for t in ("float", "double")]
          + [("ils_inst.cu", f"col_rt_{t}", [f"-DILS_INST_COL_RT={t}"]) for t in ("float", "double")]
          + [("ils_inst.cu", f"row_spec{i}", [f"-DILS_INST_ROW_SPEC={i}"]) for i in range(N_ROW_SPECS)]
-         + [("ils_inst.cu", f"col_spec{i}", [f"-DILS_INST_COL_SPEC={i}"]) for i in range(N_COL_SPECS)])
+         + [("ils_inst.cu", f"col_spec{i}", [f"-DILS_INST_COL_SPEC={i}"]) for i in range(N_COL_SPECS)]
+         + [("ils_inst.cu", "col2", ["-DILS_INST_COL2"])])
 SOURCES = sorted({u[0] for u in UNITS})
-HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_inst.cu"]
+HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_col2.cuh", "ils_inst.cu"]
+BASE_HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh"]
+
+
+def _unit_deps(src, tag):
+    """Files one object depends on (ils_col2.cuh only reaches the api and col2 units)."""
+    deps = [src] + BASE_HEADERS
+    if tag in ("api", "col2"):
+        deps.append("ils_col2.cuh")
+    deps = [os.path.join(CSRC, d) for d in deps]
+    deps.append(os.path.join(ROOT, "include", "ils_b200.h"))
+    deps.append(os.path.abspath(__file__))
+    return deps
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -58,13 +71,17 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
         return LIB
     objdir = os.path.join(HERE, "build_obj")
     os.makedirs(objdir, exist_ok=True)
-    jobs = []
+    jobs, objs = [], []
     for src, tag, defs in UNITS:
         obj = os.path.join(objdir, tag + ".o")
+        objs.append(obj)
+        if not force and not extra and os.path.exists(obj):
+            t = os.path.getmtime(obj)
+            if all(os.path.getmtime(d) <= t for d in _unit_deps(src, tag) if os.path.exists(d)):
+                continue  # object newer than everything it includes
         cmd = [_nvcc(), *NVCC_FLAGS, *extra, *defs, "-I", os.path.join(ROOT, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         jobs.append((tag, obj, cmd))
-    objs = [j[1] for j in jobs]
     nproc = max(1, min(len(jobs), os.cpu_count() or 4))
     running, failed = [], []
     for tag, obj, cmd in jobs:

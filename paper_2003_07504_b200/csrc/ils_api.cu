@@ -17,6 +17,7 @@
 
 #include "../../include/ils_b200.h"
 #include "ils_kernels.cuh"
+#include "ils_col2.cuh"
 
 using namespace ils;
 
@@ -118,6 +119,12 @@ struct SpecHost {
 const SpecHost kRowSpecs[] = {ILS_ROW_SPECS(ILS_HOST_SPEC)};
 const SpecHost kColSpecs[] = {ILS_COL_SPECS(ILS_HOST_SPEC)};
 #undef ILS_HOST_SPEC
+struct Col2Host {
+  int id, n1, n2, cw;
+};
+#define ILS_HOST_COL2(ID, N1, N2, CW, MINB) Col2Host{ID, N1, N2, CW},
+const Col2Host kCol2Specs[] = {ILS_COL2_SPECS(ILS_HOST_COL2)};
+#undef ILS_HOST_COL2
 
 // Shared-memory wavefronts of one transform relative to the conflict-free
 // ideal, for a line layout (identity or XOR swizzle), following exactly the
@@ -257,10 +264,11 @@ struct ils_plan {
   int C, CS, col_threads, col_grid;
   size_t col_smem;
   int row_spec = -1, col_spec = -1;  // compile-time FFT plan ids (-1: runtime plan)
+  int col2 = -1;                     // two-stage column solve (ILS_COL2_SPECS id), -1: k_col
   int sms = 148;                     // SMs of the plan's device (waves model)
   FftHost rowf, colf;
   void* d_tables = nullptr;
-  size_t off_rowtw, off_coltw, off_wreal, off_wx, off_wy, off_sink;  // byte offsets
+  size_t off_rowtw, off_coltw, off_wreal, off_wx, off_wy, off_tw2, off_sink;  // byte offsets
   size_t spec_bytes;                                       // one half spectrum
   size_t off_fcopy;                                        // workspace: planar f of the 8-bit path
   size_t epart_elems;                                      // doubles for trace partials
@@ -399,6 +407,12 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
   if (best == 1e300) return false;
   p.col_threads = kColThreads;
   p.col_grid = (p.Wc + p.C - 1) / p.C;
+  // the solve pass (COL_SOLVE) of fp32 plans whose height has a two-stage
+  // kernel runs k_col2; the standalone transforms keep k_col
+  p.col2 = -1;
+  if (p.dtype == ILS_F32 && !env_int("ILS_NO_SPECS", 0) && !env_int("ILS_NO_COL2", 0))
+    for (const Col2Host& c : kCol2Specs)
+      if (c.n1 * c.n2 == p.H) p.col2 = c.id;
   return true;
 }
 
@@ -490,6 +504,7 @@ ColArgs<T> col_args(const ils_plan* p, cx<T>* S, int mode) {
   a.S_ps = (long long)p->H * p->Sp;
   a.wx = reinterpret_cast<const T*>(static_cast<const char*>(p->d_tables) + p->off_wx);
   a.wy = reinterpret_cast<const T*>(static_cast<const char*>(p->d_tables) + p->off_wy);
+  a.tw2 = reinterpret_cast<const cx<T>*>(static_cast<const char*>(p->d_tables) + p->off_tw2);
   a.cl2 = T(p->prm.c * p->prm.lam / 2.0);
   a.inv_hw = T(1.0 / ((double)p->H * (double)p->W));
   a.mode = mode;
@@ -518,7 +533,24 @@ cudaError_t launch_row(const ils_plan* p, int mode, RowArgs<T> a, cudaStream_t s
 }
 
 template <typename T>
+cudaError_t launch_col2(const ils_plan* p, const ColArgs<T>& a, int planes, cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value) {
+    switch (p->col2) {
+#define ILS_CASE(ID, N1, N2, CW, MINB) \
+  case ID:                             \
+    return launch_col2_impl<N1, N2, CW, MINB>(a, planes, s);
+      ILS_COL2_SPECS(ILS_CASE)
+#undef ILS_CASE
+      default:
+        break;
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
 cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
+  if (p->col2 >= 0 && a.mode == COL_SOLVE) return launch_col2<T>(p, a, p->B, s);
   const dim3 grid(p->col_grid, p->B);
   if constexpr (std::is_same<T, float>::value) {
     switch (p->col_spec) {
@@ -733,6 +765,8 @@ ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32
   off = align(off + p->Wc * rs);
   p->off_wy = off;
   off = align(off + p->H * rs);
+  p->off_tw2 = off;
+  off = align(off + 2 * p->H * rs);
   p->off_sink = off;  // scratch status word for ils_irfft2
   off += 256;
   std::vector<double> host(off / 8 + 1, 0.0);
@@ -759,6 +793,13 @@ ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32
   put(p->off_wreal, wr);
   put(p->off_wx, wx);
   put(p->off_wy, wy);
+  std::vector<double> tw2(2 * p->H);  // exp(-2 pi i m / H)
+  for (int m = 0; m < p->H; ++m) {
+    const sc_t w = sincos2pi(-m, height);
+    tw2[2 * m] = w.c;
+    tw2[2 * m + 1] = w.s;
+  }
+  put(p->off_tw2, tw2);
   p->spec_bytes = ((size_t)batch * height * p->Sp * elt + 255) & ~size_t(255);
   p->epart_elems = (size_t)(params->iters + 1) * batch * p->row_grid;
   p->off_fcopy = (2 * p->spec_bytes + 256 + p->epart_elems * sizeof(double) + 255) & ~size_t(255);
@@ -826,6 +867,13 @@ ils_status ils_plan_get_info(const ils_plan* p, ils_plan_info* i) {
   for (size_t k = 0; k < p->colf.radix.size() && k < 16; ++k) i->col_radix[k] = p->colf.radix[k];
   i->spec_pitch = p->Sp;
   i->launches_per_call = 2 * p->prm.iters + 1;
+  i->col2_spec = p->col2;
+  for (const Col2Host& c : kCol2Specs)
+    if (c.id == p->col2) {
+      i->col2_n1 = c.n1;
+      i->col2_n2 = c.n2;
+      i->col2_cols = c.cw;
+    }
   return ILS_OK;
 }
 
@@ -1230,6 +1278,7 @@ ils_status ils_slab_plan_create(ils_plan** out, int32_t height, int32_t width, c
     p->off_wreal = full->off_wreal;
     p->off_wx = full->off_wx;
     p->off_wy = full->off_wy;
+    p->off_tw2 = full->off_tw2;
     p->off_sink = full->off_sink;
     full->d_tables = nullptr;
     ils_plan_destroy(full);
@@ -1329,6 +1378,11 @@ ils_status slab_col_t(const ils_plan* p, cx<T>* recv, cx<T>* send, cudaStream_t 
   c.dst = send;
   const dim3 grid(p->col_grid, 1);
   cudaError_t e;
+  if (p->col2 >= 0) {
+    e = launch_col2<T>(p, c, 1, s);
+    if (e != cudaSuccess) return fail(ILS_ECUDA, "slab col pass: %s", cudaGetErrorString(e));
+    return ILS_OK;
+  }
   if constexpr (std::is_same<T, float>::value) {
     switch (p->col_spec) {
 #define ILS_CASE(ID, ...)                                                                    \

@@ -4,8 +4,12 @@
 //   -DILS_INST_COL_RT=<float|double>    runtime-planned column kernel
 //   -DILS_INST_ROW_SPEC=<id>            fp32 row kernel for ILS_ROW_SPECS entry id
 //   -DILS_INST_COL_SPEC=<id>            fp32 column kernel for ILS_COL_SPECS entry id
+//   -DILS_INST_COL2                     fp32 two-stage column kernels (ILS_COL2_SPECS)
 #define ILS_DEFINE_LAUNCHERS
 #include "ils_kernels.cuh"
+#ifdef ILS_INST_COL2
+#include "ils_col2.cuh"
+#endif
 
 namespace ils {
 #ifdef ILS_INST_ROW_RT
@@ -28,5 +32,11 @@ template cudaError_t launch_row_impl<float, true, RowSpec<ILS_INST_ROW_SPEC>::ty
 #ifdef ILS_INST_COL_SPEC
 template cudaError_t launch_col_impl<float, ColSpec<ILS_INST_COL_SPEC>::type>(const ColArgs<float>&, dim3, int, size_t,
                                                                               cudaStream_t);
+#endif
+#ifdef ILS_INST_COL2
+#define ILS_CASE(ID, N1, N2, CW, MINB) \
+  template cudaError_t launch_col2_impl<N1, N2, CW, MINB>(const ColArgs<float>&, int, cudaStream_t);
+ILS_COL2_SPECS(ILS_CASE)
+#undef ILS_CASE
 #endif
 }  // namespace ils

@@ -122,6 +122,7 @@ struct ColArgs {
   cx<T>* dst;
   const T* wx;  // 2 - 2 cos(2 pi kx / W), kx < Wc
   const T* wy;  // 2 - 2 cos(2 pi ky / H)
+  const cx<T>* tw2;  // exp(-2 pi i m / H), m < H (two-stage column kernel)
   T cl2;        // c * lam / 2
   T inv_hw;     // 1 / (H W)
   int mode;
