@@ -412,7 +412,11 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
   p.col2 = -1;
   if (p.dtype == ILS_F32 && !env_int("ILS_NO_SPECS", 0) && !env_int("ILS_NO_COL2", 0))
     for (const Col2Host& c : kCol2Specs)
-      if (c.n1 * c.n2 == p.H) p.col2 = c.id;
+      if (c.n1 * c.n2 == p.H && p.col2 < 0) p.col2 = c.id;
+  const int force2 = env_int("ILS_COL2_SPEC", -1);
+  if (p.col2 >= 0 && force2 >= 0)
+    for (const Col2Host& c : kCol2Specs)
+      if (c.id == force2 && c.n1 * c.n2 == p.H) p.col2 = c.id;
   return true;
 }
 
@@ -586,11 +590,18 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
   a.u_rp = p->W;
   a.status = status;
   if (f8) {
-    a.f8 = f8;
+    // 8-bit ingest: deinterleave + v/255 into the workspace's planar f, which
+    // every row pass (F0 included) then reads as an ordinary fp32 plane
     a.ch = ch;
     a.fcopy = reinterpret_cast<T*>(static_cast<char*>(ws) + p->off_fcopy);
     a.f = a.fcopy;
     a.f_ps = (int64_t)p->H * p->W;
+    const long long npx = (long long)p->H * p->W;
+    const int frames = p->B / ch;
+    const long long work = (ch == 3 && (npx & 3) == 0) ? npx / 4 * frames : npx * frames * ch;
+    const int blocks = (int)std::min<long long>((work + 255) / 256, (long long)p->sms * 8);
+    k_u8_planar<T><<<blocks, 256, 0, s>>>(f8, a.fcopy, ch, npx, frames);
+    ILS_CUDA(cudaGetLastError());
   }
   const int iters = p->prm.iters;
   cx<T>* cur = Sa;
@@ -988,6 +999,49 @@ ils_status ils_host_io_size(const ils_plan* p, size_t* bytes) {
 
 namespace {
 
+// Streams, events and the pinned status words of the host pipeline, created
+// once per (thread, device) and reused by every call on that thread (creating
+// them per call cost about a millisecond of pinned allocation and stream
+// setup, serialised in front of every batch group).  Thread-local, so plans
+// stay shareable across threads; intentionally never freed (process exit
+// may run after the CUDA context is gone).
+struct HostRes {
+  cudaStream_t h2d = nullptr, d2h = nullptr, lane1 = nullptr;
+  cudaEvent_t ev_in[kIoSlots] = {}, ev_comp[kIoSlots] = {}, ev_out[kIoSlots] = {};
+  int32_t* hstat = nullptr;
+  int hcap = 0;
+};
+
+cudaError_t host_res(int device, int nstat, HostRes** out) {
+  static thread_local HostRes* cache[64] = {};
+  if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+  HostRes*& R = cache[device];
+  if (!R) {
+    HostRes* n = new HostRes();
+    cudaError_t e = cudaStreamCreateWithFlags(&n->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&n->d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&n->lane1, cudaStreamNonBlocking);
+    for (int i = 0; i < kIoSlots && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&n->ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&n->ev_comp[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&n->ev_out[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return e;  // partially built resources leak (error path only)
+    R = n;
+  }
+  if (R->hcap < nstat) {
+    if (R->hstat) cudaFreeHost(R->hstat);
+    R->hstat = nullptr;
+    R->hcap = 0;
+    const int cap = std::max(nstat, 64);
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&R->hstat), sizeof(int32_t) * cap, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    R->hcap = cap;
+  }
+  *out = R;
+  return cudaSuccess;
+}
+
 // Pipelined host path shared by ils_smooth_host / ils_smooth_host_u8: batch k
 // runs on compute lane k & 1 (the caller's stream with the caller's
 // workspace, or an internal stream with the second workspace carved from
@@ -1015,40 +1069,24 @@ ils_status host_pipeline(const ils_plan* p, const void* f_host, void* u_host, si
   const size_t full_slot = ((size_t)p->B * p->H * p->W * es + 255) & ~size_t(255);
   void* wsl[2] = {ws, io + 2 * NS * full_slot + 1024};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaStream_t lane[2] = {s, nullptr};
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[NS] = {}, ev_comp[NS] = {}, ev_out[NS] = {};
-  int32_t* hstat = nullptr;
   ils_status rc = ILS_OK;
-  auto cleanup = [&]() {
-    for (int i = 0; i < NS; ++i) {
-      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
-      if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
-      if (ev_out[i]) cudaEventDestroy(ev_out[i]);
-    }
-    if (h2d) cudaStreamDestroy(h2d);
-    if (d2h) cudaStreamDestroy(d2h);
-    if (lane[1]) cudaStreamDestroy(lane[1]);
-    if (hstat) cudaFreeHost(hstat);
-  };
 #define ILS_TRY(call)                                                                    \
   do {                                                                                   \
     cudaError_t e_ = (call);                                                             \
     if (e_ != cudaSuccess) {                                                             \
       rc = fail(ILS_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));                     \
-      cleanup();                                                                         \
       return rc;                                                                         \
     }                                                                                    \
   } while (0)
-  ILS_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
-  ILS_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-  ILS_TRY(cudaStreamCreateWithFlags(&lane[1], cudaStreamNonBlocking));
-  for (int i = 0; i < NS; ++i) {
-    ILS_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-    ILS_TRY(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
-    ILS_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
-  }
-  ILS_TRY(cudaHostAlloc(reinterpret_cast<void**>(&hstat), sizeof(int32_t) * nbatches, cudaHostAllocDefault));
+  int dev = 0;
+  ILS_TRY(cudaGetDevice(&dev));
+  HostRes* R = nullptr;
+  ILS_TRY(host_res(dev, nbatches, &R));
+  cudaStream_t lane[2] = {s, R->lane1};
+  cudaStream_t h2d = R->h2d, d2h = R->d2h;
+  cudaEvent_t *ev_in = R->ev_in, *ev_comp = R->ev_comp, *ev_out = R->ev_out;
+  int32_t* hstat = R->hstat;
+  auto cleanup = [] {};
   // the caller's stream may still be producing host-visible state: order h2d after it
   ILS_TRY(cudaEventRecord(ev_out[0], s));
   ILS_TRY(cudaStreamWaitEvent(h2d, ev_out[0], 0));

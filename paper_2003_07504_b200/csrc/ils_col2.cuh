@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
 }
 
 // (id, N1, N2, CW, min CTAs per SM)
-#define ILS_COL2_SPECS(X) X(0, 36, 30, 8, 2)
+#define ILS_COL2_SPECS(X) X(0, 36, 30, 8, 2) X(1, 36, 30, 6, 3) X(2, 36, 30, 4, 4) X(3, 36, 30, 10, 1) X(4, 36, 30, 10, 2) X(5, 30, 36, 8, 2) X(6, 36, 30, 16, 1)
 
 template <int N1, int N2, int CW, int MINB>
 cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s);
@@ -141,7 +141,7 @@ template <int N1, int N2, int CW, int MINB>
 cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s) {
   using S = Col2Shape<N1, N2, CW>;
   auto k = k_col2<N1, N2, CW, MINB>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+  cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), S::SMEM);
   if (e != cudaSuccess) return e;
   const dim3 grid((a.Wc + CW - 1) / CW, planes);
   k<<<grid, S::NT, S::SMEM, s>>>(a);

@@ -19,6 +19,9 @@
 
 #include "ils_fft.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace ils {
 
 enum RowMode : int {
@@ -94,8 +97,8 @@ struct RowArgs {
   const cx<T>* wreal;  // exp(-2 pi i k / W), k = 0..N/2 (packed only)
   // 8-bit interleaved frames (kernels specialised with SMODE >= kU8Modes):
   // plane b is channel b % ch of frame b / ch in [frames][H][W][ch] bytes.
-  // F0 reads f8 (v / 255, formats.py read side) and writes the planar copy
-  // fcopy the later row passes add; FIN writes u8 = floor(clip01(u) 255 + 0.5)
+  // k_u8_planar turns f8 into the planar fcopy (v / 255, formats.py read
+  // side) every row pass reads as f; FIN writes u8 = floor(clip01(u) 255 + 0.5)
   // (formats.py:25-27).
   const unsigned char* f8;
   unsigned char* u8;
@@ -426,7 +429,7 @@ constexpr int kU8Modes = 8;
 #ifndef ILS_STENCIL_ROWS
 #define ILS_STENCIL_ROWS 3
 #endif
-constexpr int kStencilRows = ILS_STENCIL_ROWS;  // SMODE = kU8Modes + MODE_F0 / MODE_FIN: 8-bit frame ingest / egress
+constexpr int kStencilRows = ILS_STENCIL_ROWS;  // SMODE = kU8Modes + MODE_FIN: 8-bit frame egress
 
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
@@ -436,8 +439,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   using Grp = GroupT<FS::G>;
   constexpr bool BULK = kBulkRows<T, FS> && PACKED;
   constexpr bool U8 = SMODE >= kU8Modes;
-  constexpr bool LOADF8 = U8 && SMODE - kU8Modes == MODE_F0;
-  constexpr bool BULKIN = BULK && !LOADF8;
+  constexpr bool BULKIN = BULK;
   constexpr bool SOFTOK = SMODE < 0 || U8;  // kernels that accept the soft-threshold penalty
   const int MODE = U8 ? SMODE - kU8Modes : (SMODE >= 0 ? SMODE : A.mode);  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         }
       }
       __syncthreads();
-    } else if (!LOADF8 && (MODE != MODE_F0 || PACKED)) {
+    } else if (MODE != MODE_F0 || PACKED) {
       for (int i = g.id; i < nl; i += ngroups) {
         const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
         cx<T>* z = L.line(i);
@@ -566,49 +568,11 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
       cx<T>* z = L.line(i);
       if constexpr (BULKIN) {
         mbar_wait(&bars[i], 0);
-      } else if (!LOADF8 && (MODE != MODE_F0 || PACKED)) {
+      } else if (MODE != MODE_F0 || PACKED) {
         cp_async_wait_keep(mine - 1 - li);
         g.sync();
       }
-      if constexpr (LOADF8) {
-        // 8-bit ingest: channel ch of an interleaved row, plus the planar copy
-        // of the band's own rows for the later passes' f-add
-        const int C = A.ch;
-        const unsigned char* src = A.f8 + ((size_t)(b / C) * H * W + (size_t)y * W) * C + (b % C);
-        T* cp = (i >= 1 && i <= nb) ? A.fcopy + (size_t)b * A.f_ps + (size_t)(y0 + i) * A.f_rp : nullptr;
-        if (C == 3 && (W & 3) == 0) {
-          // 4 pixels = 12 bytes = 3 aligned words per thread and step
-          // (rows start at multiples of 12 W bytes from the 256-aligned base)
-          const unsigned* w3 = reinterpret_cast<const unsigned*>(src - (b % C));
-          const int sh = b % C;
-#pragma unroll 4
-          for (int q = g.rank; q < W / 4; q += g.size()) {
-            const unsigned w[3] = {__ldg(w3 + 3 * q), __ldg(w3 + 3 * q + 1), __ldg(w3 + 3 * q + 2)};
-            T v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int pos = 3 * k + sh;  // byte of pixel k, channel sh
-              const unsigned wd = pos < 4 ? w[0] : (pos < 8 ? w[1] : w[2]);
-              v[k] = u8_to((wd >> (8 * (pos & 3))) & 0xffu, T{});
-              L.set(i, 4 * q + k, v[k]);
-            }
-            if (cp) {
-              if constexpr (sizeof(T) == 4) {
-                *reinterpret_cast<float4*>(cp + 4 * q) = make_float4(v[0], v[1], v[2], v[3]);
-              } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) cp[4 * q + k] = v[k];
-              }
-            }
-          }
-        } else {
-          for (int x = g.rank; x < W; x += g.size()) {
-            const T v = u8_to(__ldg(src + (size_t)x * C), T{});
-            L.set(i, x, v);
-            if (cp) cp[x] = v;
-          }
-        }
-      } else if (MODE == MODE_F0) {
+      if (MODE == MODE_F0) {
         if (!PACKED)
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
@@ -993,6 +957,46 @@ __global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long n
   }
 }
 
+// 8-bit interleaved frames [frames][H][W][ch] -> planar planes [frames][ch][H W]
+// holding v / 255 (formats.py read side, u8_to), so the first row pass reads
+// f with whole-row TMA copies like any fp32 plane.  ch = 3: one thread per 4
+// pixels -- 3 coalesced 32-bit loads, one 16-byte store per plane.
+template <typename T>
+__global__ void k_u8_planar(const unsigned char* __restrict__ f8, T* __restrict__ f, int ch, long long npx,
+                            int nframes) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (ch == 3 && (npx & 3) == 0) {
+    const long long nq = npx / 4, total = nq * nframes;
+    const unsigned* w = reinterpret_cast<const unsigned*>(f8);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += stride) {
+      const long long fr = q / nq, qi = q - fr * nq;
+      const unsigned wd[3] = {__ldg(w + 3 * q), __ldg(w + 3 * q + 1), __ldg(w + 3 * q + 2)};
+      T* out = f + fr * 3 * npx + 4 * qi;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        T v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int pos = 3 * k + c;  // byte of pixel k, channel c
+          v[k] = u8_to((wd[pos >> 2] >> (8 * (pos & 3))) & 0xffu, T{});
+        }
+        if constexpr (sizeof(T) == 4) {
+          *reinterpret_cast<float4*>(out + c * npx) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) out[c * npx + k] = v[k];
+        }
+      }
+    }
+    return;
+  }
+  const long long total = npx * nframes * ch;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
+    const long long fr = t / (npx * ch), r = t - fr * npx * ch, i = r / ch, c = r - i * ch;
+    f[(fr * ch + c) * npx + i] = u8_to(__ldg(f8 + t), T{});
+  }
+}
+
 // ------------------------------------------------------------ applications
 // gaussian_blur (applications.py:210-222): separable, radius ceil(3 sigma),
 // replicate ("nearest") edges, axis 0 then axis 1.  Sums follow scipy's
@@ -1070,6 +1074,23 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
 template <typename T, class FS>
 cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device)
+// instead of on every launch (a driver call in the per-batch host path).
+inline cudaError_t smem_attr(const void* k, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<unsigned long long, size_t> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long key = reinterpret_cast<unsigned long long>(k) * 64ull + (unsigned)dev;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[key] = smem;
+  return e;
+}
+
 #ifdef ILS_DEFINE_LAUNCHERS
 template <typename T, bool PACKED, class FS, bool WIDE>
 cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
@@ -1077,14 +1098,13 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
   auto k = k_row<T, PACKED, FS, WIDE, -1>;
   if (a.f8 || a.u8) {
     if (a.epart) return cudaErrorInvalidValue;  // no energy trace on the 8-bit path
-    if (a.mode == MODE_F0 && a.f8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_F0>;
     if (a.mode == MODE_FIN && a.u8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_FIN>;
   } else if (a.epart == nullptr && (a.pen.kind != 2 || a.mode == MODE_FIN)) {
     if (a.mode == MODE_F0) k = k_row<T, PACKED, FS, WIDE, MODE_F0>;
     if (a.mode == MODE_IT) k = k_row<T, PACKED, FS, WIDE, MODE_IT>;
     if (a.mode == MODE_FIN) k = k_row<T, PACKED, FS, WIDE, MODE_FIN>;
   }
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   k<<<grid, threads, smem, s>>>(a);
   return cudaGetLastError();
@@ -1092,7 +1112,7 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
 template <typename T, class FS>
 cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
   auto k = k_col<T, FS>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   k<<<grid, threads, smem, s>>>(a);
   return cudaGetLastError();
