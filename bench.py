@@ -15,13 +15,16 @@ value     device throughput: frames/s over all ranks, inputs resident in HBM,
           one CUDA-graph replay per step, CUDA events, max over ranks.
 e2e       the same through the C ABI with HOST buffers (ils_smooth_host_u8):
           pinned host 8-bit RGB frames (the reference's PNG/PPM pixel format)
-          -> device copies, kernels (v/255 ingest and the quantising store
-          fused into the first/last passes), device -> host copies and the
-          status readback inside the timed region, pipelined over frames.
-          e2e_f32_planes: the same with fp32 planes (ils_smooth_host).
-roofline  the dominant kernel (fused row pass, iterations >= 1) timed alone
-          with CUDA events on its stream: algorithmic bytes / time vs the
-          measured HBM copy bandwidth in MEASURED_PEAKS.json.
+          -> device copies, kernels (v/255 deinterleave ahead of the first
+          pass, the quantising store fused into the last), device -> host
+          copies and the status readback inside the timed region, pipelined
+          over frames.  e2e_f32_planes: the same with fp32 planes.
+roofline  the dominant kernel (fused row pass, iterations >= 1), CUDA events
+          around each of its launches inside the real per-frame pass
+          sequence: algorithmic bytes / time vs the measured HBM copy
+          bandwidth in MEASURED_PEAKS.json; `traffic` = ncu DRAM bytes per
+          launch (profiles/traffic.json).  `issue`: the bound that binds --
+          ncu warp instructions per launch / time vs 4 per SM per cycle.
 cpu_baseline  the oracle port (numpy/scipy, the reference's own algorithm)
           on the host cores, one frame.
 cufft     the same loop written with torch.fft.rfft2/irfft2 (cuFFT) and
@@ -58,13 +61,25 @@ def bytes_per_frame(iters=ITERS, h=H, w=W, ch=CH):
     return ch * per_plane
 
 
-def measured_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture, or None."""
+def measured_traffic(kernel, key="bytes"):
+    """Per-launch DRAM bytes (or warp instructions) of `kernel` from the committed ncu capture, or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return float(json.load(fh)[kernel]["bytes"])
+            return float(json.load(fh)[kernel][key])
     except Exception:
         return None
+
+
+def issue_roofline(kernel, ms, sms, mhz):
+    """The bound that actually binds: warp instructions per launch (ncu, committed) / event
+    time vs the issue peak (4 schedulers x 1 warp-instruction/cycle per SM at the sampled clock)."""
+    inst = measured_traffic(kernel, "warp_instructions")
+    if inst is None or not mhz:
+        return None
+    achieved = inst / (ms / 1e3)
+    peak = sms * 4 * mhz * 1e6
+    return {"achieved": round(achieved / 1e9, 1), "peak": round(peak / 1e9, 1), "unit": "G warp-inst/s",
+            "frac": round(achieved / peak, 4), "warp_instructions_per_launch": inst}
 
 
 def peaks():
@@ -450,6 +465,8 @@ def main():
 
     if rank == 0:
         bpf = bytes_per_frame()
+        clk_sum = clk.summary()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -458,21 +475,27 @@ def main():
             "config": {"workload": "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
                        "frames_per_step_per_gpu": F, "frames_per_launch_group": G, "streams": S,
                        "parallelism": f"frame-sharded x{world}", "l2": "inputs larger than L2 (F x 24.9 MB)",
-                       "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec",
-                                                          "col_cols", "col_group", "col_radix", "col_spec")}},
+                       "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec", "col2_spec",
+                                                          "col2_n1", "col2_n2", "col2_cols")}},
             "e2e": e2e,
             "e2e_f32_planes": e2e_f32,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": round(row_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(row_gbs / peak, 4), "traffic": measured_traffic("k_row_it"),
                          "traffic_source": "profiles/traffic.json (ncu --set full, warm L2)", "peak_kind": peak_kind,
+                         "issue": issue_roofline("k_row_it", ms_row, sms, clk_sum["sm_mhz"]),
                          "kernel": "k_row fused row pass (iteration>=1)", "ms": round(ms_row, 4),
                          "timing": "CUDA events around each launch inside the per-frame pass sequence (warm L2)",
                          "ms_isolated_loop": round(ms_row_isolated, 4),
                          "pass_ms_in_sequence": {"row_f0": round(seq[0], 4), "col": round(seq[1], 4),
                                                  "row_it": round(seq[2], 4), "row_fin": round(seq[3], 4)},
                          "bytes_per_launch": row_bytes,
-                         "col_pass": {"achieved": round(col_gbs, 1), "frac": round(col_gbs / peak, 4),
+                         "col_pass": {"kernel": "k_col2" if plan.info.get("col2_spec", -1) >= 0 else "k_col",
+                                      "achieved": round(col_gbs, 1), "frac": round(col_gbs / peak, 4),
+                                      "traffic": measured_traffic("k_col2" if plan.info.get("col2_spec", -1) >= 0
+                                                                  else "k_col"),
+                                      "issue": issue_roofline("k_col2", ms_col, sms, clk_sum["sm_mhz"])
+                                      if plan.info.get("col2_spec", -1) >= 0 else None,
                                       "ms": round(ms_col, 4), "ms_isolated_loop": round(ms_col_isolated, 4),
                                       "bytes_per_launch": col_bytes},
                          "whole_path": {"achieved": round(bpf * value / world / 1e9, 1),
@@ -480,7 +503,7 @@ def main():
                                         "bytes_per_frame": bpf}},
             "cpu_baseline": cpu,
             "cufft_comparison": cufft,
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
