@@ -449,7 +449,10 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * A.band;
   const int nb = min(A.band, A.H - r0);
-  const int W = A.W, H = A.H;
+  // compile-time plans fix the width (W = 2n packed): every strip bound and
+  // wrap in the stencil folds, so its per-element guards compile away
+  constexpr int WCT = (FS::n > 0 && PACKED) ? 2 * FS::n : 0;
+  const int W = WCT > 0 ? WCT : A.W, H = A.H;
   const bool trace = SMODE < 0 && A.epart != nullptr;
   const bool halo = (MODE == MODE_F0 || MODE == MODE_IT || (MODE == MODE_FIN && trace));
   const int nl = halo ? nb + 2 : nb;
@@ -667,6 +670,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     // line j once every thread is past row r0+j-1.  f of the next row is
     // prefetched into registers one row ahead.
     constexpr int QW = WIDE ? 8 : 4;
+    // every strip is whole when the compile-time width is a multiple of QW
+    constexpr bool ALLFULL = WCT > 0 && WCT % QW == 0;
     // strips per thread: exact for compile-time plans, 4 (W <= 16 * 256) otherwise
     constexpr int GMAX = FS::n > 0 ? (2 * FS::n / QW + kRowThreads - 1) / kRowThreads : 4;
     const int ng = (W + QW - 1) / QW;
@@ -706,7 +711,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
             const int gg = tid + gi * nthr;
             if (gg < ng) {
               const int x0 = gg * QW;
-              const bool full = PACKED && x0 + QW <= W;
+              const bool full = ALLFULL || (PACKED && x0 + QW <= W);
               if (TR && is_it) {
                 const T* fr = fpl + (size_t)(r0 + min(j + 1, nb - 1)) * A.f_rp + x0;
 #pragma unroll
@@ -768,7 +773,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
             const int gg = tid + gi * nthr;
             if (gg < ng) {
               const int x0 = gg * QW;
-              if (PACKED && x0 + QW <= W) {
+              if (ALLFULL || (PACKED && x0 + QW <= W)) {
                 L.template set_strip<QW>(j, x0, rhs[kk][gi]);
               } else {
 #pragma unroll
