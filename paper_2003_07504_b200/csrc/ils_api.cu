@@ -315,8 +315,10 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   // a swizzled layout permutes inside whole 128-byte blocks: round up to them
   const int E = elt == 8 ? 16 : 8;
   // interior passes swizzle elements < n inside whole 128-byte blocks
-  const int LP = std::max(p.rowf.swz ? (p.N + E - 1) / E * E : 0, (line + 1) & ~1);
-  const size_t wreal_bytes = p.packed ? (size_t)(p.N / 2 + 1) * elt : 0;  // staged twiddles
+  int LP = std::max(p.rowf.swz ? (p.N + E - 1) / E * E : 0, (line + 1) & ~1);
+  if (p.rowf.swz == 3) LP = std::max(LP, (p.N + p.N / 32 + 1) & ~1);  // padded interior layout
+  // packing twiddles staged in shared memory, except for kind-3 plans (L1)
+  const size_t wreal_bytes = (p.packed && p.rowf.swz != 3) ? (size_t)(p.N / 2 + 1) * elt : 0;
   // Band size: minimise (waves x per-CTA work).  A CTA of band b transforms
   // b+2 lines c2r and b lines r2c; 2 CTAs fit an SM while smem <= ~113 KB.
   const int force = env_int("ILS_ROW_BAND", 0);

@@ -59,14 +59,20 @@ constexpr int kSwzMask = (1 << SwzShift<T>::value) - 1;
 
 // Line layouts: kind 0 identity, 1 XOR by the 128-byte block index, 2 XOR
 // by (block index ^ block index >> 1) -- the latter suits radix-32 first
-// passes.  LayoutCt: compile-time kind (hot sizes); LayoutRt: runtime.
+// passes.  Kind 3 (compile-time two-pass 32 x R plans only) pads one slot
+// per 32 elements, L(e) = e + e/32: the radix-32 pass stores 32 j + r at
+// 33 j + r and the second pass loads j + 32 r from j + 33 r, so both are
+// conflict-free and every address is a per-thread base plus an immediate --
+// no XOR index arithmetic at all (the line needs n + n/32 slots).
+// LayoutCt: compile-time kind (hot sizes); LayoutRt: runtime (kinds 0-2).
 template <typename T, int KIND>
 struct LayoutCt {
   __device__ __forceinline__ int operator()(int e) const {
     constexpr int SH = SwzShift<T>::value, M = kSwzMask<T>;
     if constexpr (KIND == 0) return e;
     else if constexpr (KIND == 1) return e ^ ((e >> SH) & M);
-    else return e ^ (((e >> SH) ^ (e >> (SH + 1))) & M);
+    else if constexpr (KIND == 2) return e ^ (((e >> SH) ^ (e >> (SH + 1))) & M);
+    else return e + (e >> 5);
   }
 };
 template <typename T>
@@ -319,6 +325,7 @@ __device__ __forceinline__ std::conditional_t<FIRST, Pre, NoPre> pick_pre(const 
 // FftCt<SWZ, G, N, radices...>: the hot sizes -- group size, layout, n, Ns
 // and every index are compile-time constants.
 struct FftRt {
+  static constexpr int swz = 0;  // runtime layout (kinds 0-2, FftDev::laykind)
   static constexpr int n = 0;
   static constexpr int G = 0;
   static constexpr int ME = 1;  // no twiddle cache for runtime plans

@@ -331,10 +331,18 @@ __device__ __forceinline__ void bulk_wait_reads() {
 }
 
 // ------------------------------------------------------------ real <-> half-complex packing
+// packing twiddle k: from the shared-memory copy (SMEM), or -- plans whose
+// padded lines leave no room for it (layout kind 3) -- read-only global
+// memory through L1
+template <bool SMEM, typename T>
+__device__ __forceinline__ cx<T> ldw(const cx<T>* w, int k) {
+  if constexpr (SMEM) return w[k];
+  else return ldg_cx(w + k);
+}
 // Forward post-process of one packed line: Z = FFT_N(x[2n] + i x[2n+1]) ->
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
 // O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
-template <typename T, class Grp>
+template <typename T, bool SMEM, class Grp>
 __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* wreal, const Grp& g) {
   for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
@@ -346,7 +354,7 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* wreal, co
       const cx<T> E{T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y)};
       const cx<T> d{T(0.5) * (zk.x - zm.x), T(0.5) * (zk.y + zm.y)};  // (zk - conj zm)/2
       const cx<T> O{d.y, -d.x};                                          // -i * d
-      const cx<T> wO = cmul(wreal[k], O);
+      const cx<T> wO = cmul(ldw<SMEM>(wreal, k), O);
       z[k] = E + wO;
       if (N - k != k) z[N - k] = conj(E - wO);
     }
@@ -357,7 +365,7 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* wreal, co
 // Inverse pre-process: Z_k = E + iO, Z_{N-k} = conj(E) + i conj(O) with
 // E = X_k + conj X_{N-k}, O = (X_k - conj X_{N-k}) conj(w^k).  An inverse
 // N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
-template <typename T, class Grp>
+template <typename T, bool SMEM, class Grp>
 __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* wreal, const Grp& g) {
   for (int k = g.rank; k <= N / 2; k += g.size()) {
     if (k == 0) {
@@ -367,7 +375,7 @@ __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* wreal, con
       const cx<T> xk = z[k], xm = z[N - k];
       const cx<T> E{xk.x + xm.x, xk.y - xm.y};
       const cx<T> D{xk.x - xm.x, xk.y + xm.y};
-      const cx<T> O = cmulc(D, wreal[k]);
+      const cx<T> O = cmulc(D, ldw<SMEM>(wreal, k));
       z[k] = cx<T>{E.x - O.y, E.y + O.x};
       if (N - k != k) z[N - k] = cx<T>{E.x + O.y, -E.y + O.x};
     }
@@ -462,8 +470,10 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   const PenaltyDev<T>& P = A.pen;
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
   // real-packing twiddles staged in shared memory after the band's lines
-  cx<T>* swreal = reinterpret_cast<cx<T>*>(smem_raw) + (size_t)(A.band + 2) * A.LP;
-  if (PACKED) {
+  constexpr bool WSMEM = FS::swz != 3;  // kind-3 plans read them from global memory
+  cx<T>* swreal = WSMEM ? reinterpret_cast<cx<T>*>(smem_raw) + (size_t)(A.band + 2) * A.LP
+                        : const_cast<cx<T>*>(A.wreal);
+  if (PACKED && WSMEM) {
     for (int k = tid; k <= A.N / 2; k += nthr) swreal[k] = A.wreal[k];
     __syncthreads();
   }
@@ -580,7 +590,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
         if (PACKED) {
-          c2r_pre<T>(z, A.N, swreal, g);
+          c2r_pre<T, WSMEM>(z, A.N, swreal, g);
         } else {
           // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
           for (int k = A.Wc + g.rank; k < W; k += g.size()) z[k] = conj(z[W - k]);
@@ -810,7 +820,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         for (int x = g.rank; x < W; x += g.size()) z[x].x += fpl[(size_t)(r0 + i) * A.f_rp + x];
       fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
     }
-    if (PACKED) r2c_post<T>(z, A.N, swreal, g);
+    if (PACKED) r2c_post<T, WSMEM>(z, A.N, swreal, g);
     else g.sync();
     if (A.sout_seg.n == 0) {
       cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
@@ -1052,7 +1062,7 @@ __global__ void k_gauss_rows(const T* __restrict__ x, T* __restrict__ y, int W, 
 // runtime-planned path (FftRt).  The host planner (ils_api.cu) uses exactly
 // these radix lists when n matches, so twiddle tables and kernels agree.
 // X(id, swizzle, group threads, elements per thread, n, radices...)
-#define ILS_ROW_SPECS(X) X(0, 1, 32, 16, 256, 16, 16) X(1, 2, 32, 32, 960, 32, 30) X(2, 1, 128, 16, 1920, 16, 15, 8) X(3, 1, 256, 16, 3840, 16, 16, 15) X(4, 1, 32, 16, 512, 16, 8, 4)
+#define ILS_ROW_SPECS(X) X(0, 1, 32, 16, 256, 16, 16) X(1, 3, 32, 32, 960, 32, 30) X(2, 1, 128, 16, 1920, 16, 15, 8) X(3, 1, 256, 16, 3840, 16, 16, 15) X(4, 1, 32, 16, 512, 16, 8, 4)
 // row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
 #define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)
 #define ILS_COL_SPECS(X) X(0, 1, 32, 16, 512, 16, 8, 4) X(1, 0, 128, 16, 1080, 9, 12, 10) X(2, 1, 256, 16, 2160, 16, 15, 9) X(3, 1, 32, 16, 256, 16, 16) X(4, 1, 128, 16, 720, 16, 9, 5) X(5, 1, 256, 24, 4320, 24, 18, 10)
