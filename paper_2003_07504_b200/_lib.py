@@ -14,7 +14,8 @@ import threading
 from .errors import NumericalError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libils_b200.so")
+# ILS_LIB: an alternative build of the same library (tuning variants, tools/build_variant.py)
+LIB_PATH = os.environ.get("ILS_LIB") or os.path.join(HERE, "libils_b200.so")
 
 ILS_OK, ILS_EINVAL, ILS_ENONFINITE_INPUT, ILS_ENONFINITE, ILS_ECUDA, ILS_EUNSUPPORTED = range(6)
 ILS_CHARBONNIER, ILS_WELSCH, ILS_SOFT = 0, 1, 2

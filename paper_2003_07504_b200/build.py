@@ -25,7 +25,7 @@ UNITS = ([("ils_api.cu", "api", [])]
          + [("ils_inst.cu", f"col_rt_{t}", [f"-DILS_INST_COL_RT={t}"]) for t in ("float", "double")]
          + [("ils_inst.cu", f"row_spec{i}", [f"-DILS_INST_ROW_SPEC={i}"]) for i in range(N_ROW_SPECS)]
          + [("ils_inst.cu", f"col_spec{i}", [f"-DILS_INST_COL_SPEC={i}"]) for i in range(N_COL_SPECS)]
-         + [("ils_inst.cu", "col2", ["-DILS_INST_COL2"])])
+         + [("ils_inst.cu", "col2", ["-DILS_INST_COL2", "-DILS_PACKED_F32X2"])])
 SOURCES = sorted({u[0] for u in UNITS})
 HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_col2.cuh", "ils_inst.cu"]
 BASE_HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh"]

@@ -38,6 +38,45 @@ __host__ __device__ __forceinline__ cx<T> conj(cx<T> a) { return {a.x, -a.y}; }
 template <typename T>
 __host__ __device__ __forceinline__ cx<T> scale(cx<T> a, T s) { return {a.x * s, a.y * s}; }
 
+// fp32 complex arithmetic on sm_100's packed FP32x2 pipe (FADD2 / FMUL2 /
+// FFMA2): one instruction per complex add, two per complex multiply, with
+// swaps, sign flips and scalar broadcasts folded into operand modifiers.
+// Each lane computes exactly the scalar operations (same IEEE roundings),
+// at half the issued instructions.  Enabled per translation unit
+// (-DILS_PACKED_F32X2): it pays in the register-light column kernel; in the
+// 128-register row kernels the paired-register allocation spills and the
+// longer packed latency exposes dependency stalls (measured slower).
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000) && defined(ILS_PACKED_F32X2)
+#define ILS_F32X2 1
+__device__ __forceinline__ float2 f2_(cx<float> a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ cx<float> c2_(float2 a) { return cx<float>{a.x, a.y}; }
+__device__ __forceinline__ cx<float> operator+(cx<float> a, cx<float> b) { return c2_(__fadd2_rn(f2_(a), f2_(b))); }
+__device__ __forceinline__ cx<float> operator-(cx<float> a, cx<float> b) {
+  return c2_(__fadd2_rn(f2_(a), make_float2(-b.x, -b.y)));
+}
+// a w = w.x a + w.y (i a)
+__device__ __forceinline__ cx<float> cmul(cx<float> a, cx<float> w) {
+  const float2 t = __fmul2_rn(f2_(a), make_float2(w.x, w.x));
+  return c2_(__ffma2_rn(make_float2(-a.y, a.x), make_float2(w.y, w.y), t));
+}
+// a conj(w) = w.x a - w.y (i a)
+__device__ __forceinline__ cx<float> cmulc(cx<float> a, cx<float> w) {
+  const float2 t = __fmul2_rn(f2_(a), make_float2(w.x, w.x));
+  return c2_(__ffma2_rn(make_float2(a.y, -a.x), make_float2(w.y, w.y), t));
+}
+__device__ __forceinline__ cx<float> scale(cx<float> a, float s) { return c2_(__fmul2_rn(f2_(a), make_float2(s, s))); }
+// acc + x * s (real s)
+__device__ __forceinline__ cx<float> fma_cs(cx<float> x, float s, cx<float> acc) {
+  return c2_(__ffma2_rn(f2_(x), make_float2(s, s), f2_(acc)));
+}
+#else
+#define ILS_F32X2 0
+#endif
+template <typename T>
+__host__ __device__ __forceinline__ cx<T> fma_cs(cx<T> x, T s, cx<T> acc) {
+  return {acc.x + x.x * s, acc.y + x.y * s};
+}
+
 // ------------------------------------------------------------ constexpr trig
 constexpr double kPi = 3.141592653589793238462643383279502884;
 
@@ -150,6 +189,12 @@ __device__ __forceinline__ cx<T> twc(cx<T> a) {
   } else {
     constexpr sc_t w = sincos2pi(DIR * k, R);
     const T c = T(w.c), s = T(w.s);
+#if ILS_F32X2
+    if constexpr (std::is_same<T, float>::value) {  // c a + s (i a): FMUL2 + FFMA2, immediates
+      const float2 t = __fmul2_rn(f2_(a), make_float2(c, c));
+      return c2_(__ffma2_rn(make_float2(-a.y, a.x), make_float2(s, s), t));
+    }
+#endif
     return cx<T>{a.x * c - a.y * s, a.x * s + a.y * c};
   }
 }
@@ -179,10 +224,8 @@ __device__ __forceinline__ void dft_prime(cx<T>* v) {
       constexpr int n = ILS_CV(I) + 1;
       constexpr sc_t w = sincos2pi((long long)(n * k) % R, R);
       const T c = T(w.c), sn = T(w.s);
-      a.x += s[ILS_CV(I)].x * c;
-      a.y += s[ILS_CV(I)].y * c;
-      b.x += d[ILS_CV(I)].x * sn;
-      b.y += d[ILS_CV(I)].y * sn;
+      a = fma_cs(s[ILS_CV(I)], c, a);
+      b = fma_cs(d[ILS_CV(I)], sn, b);
     });
     const cx<T> ib = (DIR > 0) ? cx<T>{-b.y, b.x} : cx<T>{b.y, -b.x};
     out[k] = a + ib;
