@@ -329,7 +329,11 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
     if (smem > 227 * 1024) break;
     // resident CTAs/SM: register budget (kRowBlocksOf: 3 for <= 16 elements per
     // thread compile-time plans) and 228 KB of shared memory
-    const int reg_cap = (p.row_spec >= 0 && spec_me(kRowSpecs, p.row_spec) <= 16) ? 3 : 2;
+#ifdef ILS_ROW_MINB
+    const int reg_cap = ILS_ROW_MINB;
+#else
+    const int reg_cap = p.row_spec >= 0 ? 3 : 2;
+#endif
     const int per_sm = (int)std::min<size_t>(reg_cap, (228 * 1024) / (smem + 1024));
     const long ctas = (long)p.B * ((p.H + band - 1) / band);
     // issue-bound: time ~ the busiest SM's work (b+2 c2r, b r2c, b stencil rows)
