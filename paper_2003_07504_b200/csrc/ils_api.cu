@@ -602,11 +602,11 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
     a.fcopy = reinterpret_cast<T*>(static_cast<char*>(ws) + p->off_fcopy);
     a.f = a.fcopy;
     a.f_ps = (int64_t)p->H * p->W;
-    const long long npx = (long long)p->H * p->W;
+    const int npx = p->H * p->W;
     const int frames = p->B / ch;
-    const long long work = (ch == 3 && (npx & 3) == 0) ? npx / 4 * frames : npx * frames * ch;
-    const int blocks = (int)std::min<long long>((work + 255) / 256, (long long)p->sms * 8);
-    k_u8_planar<T><<<blocks, 256, 0, s>>>(f8, a.fcopy, ch, npx, frames);
+    const long long work = (ch == 3 && (npx & 3) == 0) ? npx / 4 : (long long)npx * ch;  // per frame
+    const int bx = (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, (long long)p->sms * 8 / frames));
+    k_u8_planar<T><<<dim3(bx, frames), 256, 0, s>>>(f8, a.fcopy, ch, npx);
     ILS_CUDA(cudaGetLastError());
   }
   const int iters = p->prm.iters;

@@ -986,16 +986,16 @@ __global__ void k_rgb_yuv(T* __restrict__ p, long long plane_stride, long long n
 // f with whole-row TMA copies like any fp32 plane.  ch = 3: one thread per 4
 // pixels -- 3 coalesced 32-bit loads, one 16-byte store per plane.
 template <typename T>
-__global__ void k_u8_planar(const unsigned char* __restrict__ f8, T* __restrict__ f, int ch, long long npx,
-                            int nframes) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
+__global__ void k_u8_planar(const unsigned char* __restrict__ f8, T* __restrict__ f, int ch, int npx) {
+  // blockIdx.y = frame; 32-bit indices inside a frame (no 64-bit division)
+  const size_t fr = blockIdx.y;
+  const int stride = gridDim.x * blockDim.x;
   if (ch == 3 && (npx & 3) == 0) {
-    const long long nq = npx / 4, total = nq * nframes;
-    const unsigned* w = reinterpret_cast<const unsigned*>(f8);
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += stride) {
-      const long long fr = q / nq, qi = q - fr * nq;
+    const int nq = npx / 4;
+    const unsigned* w = reinterpret_cast<const unsigned*>(f8 + fr * 3 * (size_t)npx);
+    T* out = f + fr * 3 * (size_t)npx;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
       const unsigned wd[3] = {__ldg(w + 3 * q), __ldg(w + 3 * q + 1), __ldg(w + 3 * q + 2)};
-      T* out = f + fr * 3 * npx + 4 * qi;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         T v[4];
@@ -1004,20 +1004,22 @@ __global__ void k_u8_planar(const unsigned char* __restrict__ f8, T* __restrict_
           const int pos = 3 * k + c;  // byte of pixel k, channel c
           v[k] = u8_to((wd[pos >> 2] >> (8 * (pos & 3))) & 0xffu, T{});
         }
+        T* o = out + (size_t)c * npx + 4 * q;
         if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<float4*>(out + c * npx) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) out[c * npx + k] = v[k];
+          for (int k = 0; k < 4; ++k) o[k] = v[k];
         }
       }
     }
     return;
   }
-  const long long total = npx * nframes * ch;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += stride) {
-    const long long fr = t / (npx * ch), r = t - fr * npx * ch, i = r / ch, c = r - i * ch;
-    f[(fr * ch + c) * npx + i] = u8_to(__ldg(f8 + t), T{});
+  const unsigned char* src = f8 + fr * (size_t)ch * npx;
+  T* out = f + fr * (size_t)ch * npx;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < npx * ch; t += stride) {
+    const int i = t / ch, c = t - i * ch;
+    out[(size_t)c * npx + i] = u8_to(__ldg(src + t), T{});
   }
 }
 
