@@ -449,7 +449,11 @@ constexpr int kU8Modes = 8;
 constexpr int kStencilRows = ILS_STENCIL_ROWS;  // SMODE = kU8Modes + MODE_FIN: 8-bit frame egress
 
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
+#ifdef ILS_ROW_MAXREG  // (tuning override: explicit register cap for the row kernels)
+__global__ void __maxnreg__(ILS_ROW_MAXREG) k_row(const RowArgs<T> A) {
+#else
 __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
+#endif
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[32];
   __shared__ unsigned long long bars[kMaxBandLines];

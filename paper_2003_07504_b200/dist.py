@@ -158,6 +158,60 @@ class SlabSmoother:
         return u
 
 
+def torch_exchange_async(group=None):
+    """Non-blocking all-to-all: returns the work handle (NCCL: `wait()` makes the
+    current CUDA stream wait for the exchange, the host does not block)."""
+    import torch.distributed as dist
+
+    def run(send, recv, send_counts, recv_counts):
+        return dist.all_to_all_single(recv, send, recv_counts, send_counts, group=group, async_op=True)
+
+    return run
+
+
+class SlabPipeline:
+    """C5 with the exchanges overlapped: the planes (colour channels) of one image
+    move through the slab passes as a software pipeline ("pipeline
+    the 3 channels").  While plane c's all-to-all is in flight -- NCCL runs it
+    on its own stream, `async_op=True` -- the next planes' row or column passes
+    run on the compute stream; plane c's next pass waits only for its own
+    exchange (`work.wait()` orders the compute stream after it).  Each plane has
+    its own send/receive buffers; the kernels and the exchange blocks are the
+    SlabSmoother's, so every plane's result is bit-identical to it.
+    """
+
+    def __init__(self, layout: SlabLayout, iters: int, kernels, exchange_async, alloc, planes=3,
+                 real_per_complex=2):
+        self.lay, self.iters, self.k, self.x = layout, iters, kernels, exchange_async
+        self.planes = [SlabSmoother(layout, iters, kernels, None, alloc, real_per_complex) for _ in range(planes)]
+
+    def _fwd(self, s):
+        return self.x(s.fwd_send, s.fwd_recv, s.fwd_sc, s.fwd_rc)
+
+    def _rev(self, s):
+        return self.x(s.rev_send, s.rev_recv, s.rev_sc, s.rev_rc)
+
+    def smooth(self, f_exts, us, status):
+        k, P = self.k, self.planes
+        pend = []
+        for c, s in enumerate(P):
+            k.row(0, f_exts[c], None, s.fwd_send, None, 0, status)
+            pend.append(self._fwd(s))  # plane c's transpose overlaps plane c+1's row pass
+        for n in range(self.iters):
+            for c, s in enumerate(P):
+                pend[c].wait()
+                k.col(s.fwd_recv, s.rev_send)
+                pend[c] = self._rev(s)
+            for c, s in enumerate(P):
+                pend[c].wait()
+                if n + 1 < self.iters:
+                    k.row(1, f_exts[c], s.rev_recv, s.fwd_send, None, n + 1, status)
+                    pend[c] = self._fwd(s)
+                else:
+                    k.row(3, f_exts[c], s.rev_recv, None, us[c], self.iters, status)
+        return us
+
+
 class EmulatedSlab:
     """All P ranks of a slab decomposition on ONE GPU, in lockstep.
 

@@ -114,11 +114,36 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-def _run_world(world, cases):
+def _worker_pipeline(rank, world, port, cases, q):
+    """SlabPipeline: the planes of one image with overlapped (async) exchanges."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for ci, (H, W, pen_kind) in enumerate(cases):
+            pen = Charbonnier(0.8, 1e-4) if pen_kind == 0 else Welsch(0.2)
+            params = SmoothParams(pen, 1.5, iters=3)
+            plan, lay = D.slab_layout(H, W, params.c_params(), _lib.ILS_F64, world, rank, device=-1)
+            _lib.lib().ils_plan_destroy(plan)
+            rows = D.halo_rows(H, lay.row0[rank], lay.row0[rank + 1])
+            planes = [np.random.default_rng(11 + c).random((H, W)) for c in range(3)]
+            f_exts = [torch.from_numpy(np.ascontiguousarray(p[rows])) for p in planes]
+            kern = RefSlabKernels(lay, pen, params.lam, params.curvature)
+            pipe = D.SlabPipeline(lay, params.iters, kern, D.torch_exchange_async(),
+                                  lambda n: torch.zeros(n, dtype=torch.float64), planes=3)
+            us = [torch.zeros((lay.rows, W), dtype=torch.float64) for _ in range(3)]
+            status = [_lib.STATUS_CLEAN]
+            pipe.smooth(f_exts, us, status)
+            q.put((ci, rank, lay.row0[rank], np.stack([u.numpy() for u in us]), status[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world, cases, target=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    procs = [ctx.Process(target=target or _worker, args=(r, world, port, cases, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = {}
@@ -145,6 +170,22 @@ def test_slab_driver_matches_single_image_oracle(world, cases):
         ref = O.smooth_plane(f, spec, 1.5, 4)
         assert u.shape == ref.shape
         assert np.max(np.abs(u - ref)) < 1e-12, (H, W, world)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_pipeline_overlapped_planes_match_oracle(world):
+    from oracle import ils_oracle as O
+
+    cases = [(18, 16, 0)]
+    got = _run_world(world, cases, target=_worker_pipeline)
+    H, W, _ = cases[0]
+    parts = sorted(got[0], key=lambda t: t[0])
+    u = np.concatenate([p[1] for p in parts], axis=1)  # [3, H, W]
+    assert all(p[2] == _lib.STATUS_CLEAN for p in parts)
+    for c in range(3):
+        f = np.random.default_rng(11 + c).random((H, W))
+        ref = O.smooth_plane(f, O.Charbonnier(0.8, 1e-4), 1.5, 3)
+        assert np.max(np.abs(u[c] - ref)) < 1e-12, (world, c)
 
 
 def test_frame_shard_partitions():

@@ -294,3 +294,45 @@ def test_c5_8k_texture_slab_and_wide_rows():
     uc = ils.smooth_plane(fc, params)
     ref = O.smooth_plane(fc, O.Welsch(10 / 255), 30.0, 10, c=2.0)
     assert np.max(np.abs(uc - ref)) <= 1e-4
+
+
+def test_slab_pipeline_nccl_one_rank_bitwise():
+    # C5 driver with the exchanges overlapped (SlabPipeline, async NCCL
+    # all_to_all_single on a 1-rank group): bit-identical to the 1-GPU smooth
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2003_07504_b200 import _lib
+    from paper_2003_07504_b200 import dist as D
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        H, W = 360, 640
+        params = ils.SmoothParams(ils.Welsch(10 / 255), 30.0, iters=5, c=2.0)
+        img = torch.from_numpy(np.random.default_rng(5).random((3, H, W))).to("cuda", torch.float32)
+        plan, lay = D.slab_layout(H, W, params.c_params(), _lib.ILS_F32, 1, 0, device=0)
+        stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+        pipe = D.SlabPipeline(lay, params.iters, D.CudaSlabKernels(plan, stream), D.torch_exchange_async(),
+                              lambda n: torch.zeros(n, dtype=torch.float32, device="cuda"), planes=3)
+        rows = D.halo_rows(H, 0, H)
+        f_ext = [img[c][rows].contiguous() for c in range(3)]
+        us = [torch.empty((H, W), device="cuda") for _ in range(3)]
+        status = torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device="cuda")
+        pipe.smooth(f_ext, us, status)
+        torch.cuda.synchronize()
+        assert int(status.item()) == _lib.STATUS_CLEAN
+        ref = ils.smooth_batch(img, params)
+        for c in range(3):
+            assert torch.equal(us[c], ref[c])
+        _lib.lib().ils_plan_destroy(plan)
+    finally:
+        if own:
+            dist.destroy_process_group()
