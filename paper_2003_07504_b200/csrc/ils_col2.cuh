@@ -57,15 +57,17 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
   const bool actA = r < N2;  // stages A and C: r = n2
 
   // ---------------- stage A: strided rows -> DFT_N1 -> twiddle -> smem
+  pdl_trigger();
+  for (int m = t; m < H; m += S::NT) {  // constant tables: before the wait on the previous pass
+    stw[m] = ldg_cx(A.tw2 + m);
+    swy[m] = __ldg(A.wy + m);
+  }
+  pdl_wait();
   cx<float> v[N1];
   if (actA) {
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1)
       v[n1] = colok ? ldg_cx(Spl + (size_t)(r + N2 * n1) * A.S_rp) : cx<float>{0.f, 0.f};
-  }
-  for (int m = t; m < H; m += S::NT) {
-    stw[m] = ldg_cx(A.tw2 + m);
-    swy[m] = __ldg(A.wy + m);
   }
   __syncthreads();
   if (actA) {
@@ -148,8 +150,7 @@ cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s
   cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), S::SMEM);
   if (e != cudaSuccess) return e;
   const dim3 grid((a.Wc + CW - 1) / CW, planes);
-  k<<<grid, S::NT, S::SMEM, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, S::NT, S::SMEM, s, a);
 }
 #endif
 

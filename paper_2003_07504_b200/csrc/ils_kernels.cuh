@@ -263,6 +263,15 @@ __device__ __forceinline__ void cp_async_wait_keep(int keep) {
   }
 }
 
+// ------------------------------------------------------------ programmatic dependent launch
+// The passes are launched with programmatic stream serialisation: each CTA
+// lets the next pass launch as soon as it is resident (every CTA of this
+// grid has started), the next pass stages its constant tables / twiddle
+// cache, then waits for this grid's completion (and memory flush) before it
+// touches the data this pass produces.  Both are no-ops in a normal launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------ TMA bulk copies
 // 1-D bulk copies (cp.async.bulk, SASS UBLKCP) of whole rows between global
 // memory and shared memory, completion tracked by an mbarrier (loads) or a
@@ -503,6 +512,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   TwCache<T, FS> twc;
   fill_twcache(twc, A.fft, g);
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
+  pdl_trigger();
+  pdl_wait();  // the previous pass's spectrum / the caller's f from here on
 
   if (MODE == MODE_IT && tid < nb && (W * sizeof(T)) % 16 == 0 && (A.f_rp * sizeof(T)) % 16 == 0) {
     // the stencil reads f one row at a time: pull the band's rows into L2 now
@@ -942,6 +953,8 @@ __global__ void __launch_bounds__(kColThreads, kColBlocksOf<FS>) k_col(const Col
   cx<T>* Spl = A.S + (size_t)b * A.S_ps + c0;
   TwCache<T, FS> twc;
   fill_twcache(twc, A.fft, g);
+  pdl_trigger();
+  pdl_wait();
   // transposing copies: thread -> (column cc, first row y0), rows step ystep
   const int ystep = nthr / nc, cc = tid % nc, y0 = tid / nc;
   const bool copier = tid < ystep * nc;
@@ -1147,6 +1160,27 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
 template <typename T, class FS>
 cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 
+// Launch a pass with programmatic stream serialisation (see pdl_wait);
+// ILS_NO_PDL=1 launches plainly (A/B comparisons).
+template <class K, class Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, int threads, size_t smem, cudaStream_t s, const Args& a) {
+  static const bool off = [] {
+    const char* v = getenv("ILS_NO_PDL");
+    return v && atoi(v) != 0;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 // Raise a kernel's dynamic shared-memory limit once per (kernel, device)
 // instead of on every launch (a driver call in the per-batch host path).
 inline cudaError_t smem_attr(const void* k, size_t smem) {
@@ -1179,16 +1213,14 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
   }
   cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, threads, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, threads, smem, s, a);
 }
 template <typename T, class FS>
 cudaError_t launch_col_impl(const ColArgs<T>& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
   auto k = k_col<T, FS>;
   cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, threads, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, threads, smem, s, a);
 }
 #endif
 
