@@ -76,6 +76,47 @@ def test_hot_sizes_use_compile_time_plans():
     _lib.lib().ils_plan_destroy(p)
 
 
+@pytest.mark.parametrize("h,w,n1n2", [(1080, 1920, (30, 36)), (2160, 3840, (45, 48)), (4320, 7680, (72, 60)),
+                                      (512, 512, None)])
+def test_column_solve_kernel_choice(h, w, n1n2):
+    # heights with a two-stage split run k_col2 (fp32); the 1080p row plan is
+    # the padded 32 x 30 plan budgeted for 3 CTAs per SM (band 6)
+    prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
+    st, p = _host_plan(3, h, w, prm)
+    assert st == 0
+    info = _lib.PlanInfo()
+    _lib.lib().ils_plan_get_info(p, C.byref(info))
+    d = info.as_dict()
+    if n1n2 is None:
+        assert d["col2_spec"] == -1
+    else:
+        assert d["col2_spec"] >= 0 and (d["col2_n1"], d["col2_n2"]) == n1n2
+        assert d["col2_n1"] * d["col2_n2"] == h
+    if (h, w) == (1080, 1920):
+        assert d["row_radix"] == [32, 30] and d["row_swz"] == 3 and d["row_band"] == 6
+        assert 3 * (d["row_smem"] + 1024) <= 228 * 1024
+    _lib.lib().ils_plan_destroy(p)
+    st, p64 = _host_plan(3, h, w, prm, _lib.ILS_F64)
+    if st == 0:  # (fp64 8K rows exceed the row kernel's shared memory: no fp64 plan there)
+        info = _lib.PlanInfo()
+        assert _lib.lib().ils_plan_get_info(p64, C.byref(info)) == 0
+        assert info.col2_spec == -1  # fp64 keeps the Stockham column kernel
+        _lib.lib().ils_plan_destroy(p64)
+
+
+def test_u8_ingest_newton_division_is_exact():
+    # k_u8_planar's v/255: q = v*(1/255), q += fma(-q, 255, v) * (1/255) -- equal to the
+    # correctly rounded fp32 v/255 for every byte (emulated with exact float64 FMAs)
+    v = np.arange(256, dtype=np.float32)
+    exact = (v.astype(np.float64) / 255.0).astype(np.float32)
+    r = np.float32(1.0) / np.float32(255.0)
+    q = (v * r).astype(np.float32)
+    res = (v.astype(np.float64) - q.astype(np.float64) * 255.0).astype(np.float32)
+    q2 = (res.astype(np.float64) * np.float64(r) + q.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(q2, exact)
+    assert not np.array_equal(q, exact)  # the plain reciprocal product is not
+
+
 def test_unsupported_prime_and_bad_params_map_to_valueerror():
     prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
     st, _ = _host_plan(1, 1031, 64, prm)
