@@ -177,8 +177,8 @@ def smooth_color(img: MultiImage, params: SmoothParams, trace: bool = False, wor
     if img.space == GRAY:
         res = smooth_plane(img.channels[0], params, trace, workers=workers, precision=precision)
         if trace:
-            return MultiImage((res[0],), GRAY), res[1]
-        return MultiImage((res,), GRAY)
+            return MultiImage._trusted((res[0],), GRAY), res[1]
+        return MultiImage._trusted((res,), GRAY)
     planes = rt.to_device_planes(img.channels, precision)
     cp = params.c_params()
     if params.color_mode is ColorMode.LUMINANCE_ONLY:
@@ -186,12 +186,12 @@ def smooth_color(img: MultiImage, params: SmoothParams, trace: bool = False, wor
         u, en, _ = rt.smooth_device(planes[0:1], cp, trace=trace, check=True)
         planes[0:1] = u
         rt.rgb_yuv_(planes, inverse=True)
-        out = MultiImage(tuple(rt.to_host_f64(planes)), RGB)
+        out = MultiImage._trusted(rt.to_host_f64(planes), RGB)
         if trace:
             return out, EnergyTrace([float(v) for v in en[:, 0].tolist()])
         return out
     u, en, _ = rt.smooth_device(planes, cp, trace=trace, check=True)
-    out = MultiImage(tuple(rt.to_host_f64(u)), RGB)
+    out = MultiImage._trusted(rt.to_host_f64(u), RGB)
     if trace:
         summed = [float(sum(row)) for row in en.tolist()]
         return out, EnergyTrace(summed)
