@@ -525,7 +525,15 @@ ColArgs<T> col_args(const ils_plan* p, cx<T>* S, int mode) {
 template <typename T>
 cudaError_t launch_row(const ils_plan* p, int mode, RowArgs<T> a, cudaStream_t s) {
   a.mode = mode;
-  const dim3 grid(p->row_grid, p->B);
+  // the final pass without energy trace needs no halo rows: it fills the
+  // band's 2 halo line slots with 2 more rows of its own (same shared memory,
+  // one CTA transforms band + 2 lines in the same round of line groups)
+  int gx = p->row_grid;
+  if (mode == MODE_FIN && a.epart == nullptr) {
+    a.band = p->band + 2;
+    gx = (p->H + a.band - 1) / a.band;
+  }
+  const dim3 grid(gx, p->B);
   if constexpr (std::is_same<T, float>::value) {
     switch (p->row_spec) {
 #define ILS_CASE(ID, ...) \

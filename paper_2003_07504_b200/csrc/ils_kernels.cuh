@@ -503,7 +503,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
   // real-packing twiddles staged in shared memory after the band's lines
   constexpr bool WSMEM = FS::swz != 3;  // kind-3 plans read them from global memory
-  cx<T>* swreal = WSMEM ? reinterpret_cast<cx<T>*>(smem_raw) + (size_t)(A.band + 2) * A.LP
+  // (after the band's line slots: band + 2 with halo rows, band without --
+  // the final pass runs a band 2 rows taller in the same shared memory)
+  cx<T>* swreal = WSMEM ? reinterpret_cast<cx<T>*>(smem_raw) + (size_t)(A.band + (halo ? 2 : 0)) * A.LP
                         : const_cast<cx<T>*>(A.wreal);
   if (PACKED && WSMEM) {
     for (int k = tid; k <= A.N / 2; k += nthr) swreal[k] = A.wreal[k];

@@ -6,6 +6,3 @@ timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --cache
 timeout 300 python tools/e2e_probe.py > gpurun_out/e2e_probe.log 2>&1
 timeout 600 python bench.py --steps 50 --no-cpu --no-cufft > gpurun_out/bench_quick.log 2>&1
 true
-ILS_NO_CLUSTER=1 timeout 600 python bench.py --steps 50 --no-cpu --no-cufft > gpurun_out/bench_quick_nocl.log 2>&1
-timeout 600 python tools/bench_c4.py --frames 128 > gpurun_out/c4q.log 2>&1
-timeout 600 python tools/bench_c5.py --steps 10 >> gpurun_out/c4q.log 2>&1
