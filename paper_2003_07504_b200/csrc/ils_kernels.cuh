@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   constexpr bool BULKIN = BULK;
   // specialised fp32 final pass (no trace, no 8-bit egress): each line group
   // checks and stores its own row as soon as its transform is done
-  constexpr bool FINLINE = SMODE == MODE_FIN && BULK && sizeof(T) == 4;
+  constexpr bool FINLINE8 = SMODE == kU8Modes + MODE_FIN && BULK && sizeof(T) == 4;  // same, 8-bit egress
+  constexpr bool FINLINE = (SMODE == MODE_FIN && BULK && sizeof(T) == 4) || FINLINE8;
   constexpr bool SOFTOK = SMODE < 0 || U8;  // kernels that accept the soft-threshold penalty
   const int MODE = U8 ? SMODE - kU8Modes : (SMODE >= 0 ? SMODE : A.mode);  // block-uniform
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -640,6 +641,23 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           // the optional detail/clip epilogue, and its bulk store -- no block
           // barrier between the transforms and the stores
           T* zr = reinterpret_cast<T*>(z);
+          if constexpr (FINLINE8) {
+            // quantised bytes straight to channel ch of the interleaved frame row
+            const int C = A.ch;
+            unsigned char* row = A.u8 + ((size_t)(b / C) * H + (r0 + i)) * (size_t)W * C + (b % C);
+            for (int x = 4 * g.rank; x < W; x += 4 * g.size()) {
+              const float4 q = *reinterpret_cast<const float4*>(zr + x);
+              chkf = fma_rn(q.x, T(0), chkf);
+              chkf = fma_rn(q.y, T(0), chkf);
+              chkf = fma_rn(q.z, T(0), chkf);
+              chkf = fma_rn(q.w, T(0), chkf);
+              row[(size_t)x * C] = quant8(q.x);
+              row[(size_t)(x + 1) * C] = quant8(q.y);
+              row[(size_t)(x + 2) * C] = quant8(q.z);
+              row[(size_t)(x + 3) * C] = quant8(q.w);
+            }
+            continue;
+          }
           const T* fr = fpl ? fpl + (size_t)(r0 + i) * A.f_rp : nullptr;
           for (int x = 4 * g.rank; x < W; x += 4 * g.size()) {
             float4 q = *reinterpret_cast<const float4*>(zr + x);
