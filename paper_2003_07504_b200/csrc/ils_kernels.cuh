@@ -516,13 +516,15 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   fill_twcache(twc, A.fft, g);
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
   pdl_trigger();
-  pdl_wait();  // the previous pass's spectrum / the caller's f from here on
-
   if (MODE == MODE_IT && tid < nb && (W * sizeof(T)) % 16 == 0 && (A.f_rp * sizeof(T)) % 16 == 0) {
     // the stencil reads f one row at a time: pull the band's rows into L2 now
+    // (f is the call's input, written before the first pass: no need to wait
+    // for the previous pass before the prefetch)
     const T* row = fpl + (size_t)(r0 + tid) * A.f_rp;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((unsigned)(W * sizeof(T))) : "memory");
   }
+  pdl_wait();  // the previous pass's spectrum / the caller's f from here on
+
   if (MODE == MODE_MU || MODE == MODE_R2C) {
     // rhs rows straight from global memory; each group owns whole lines.
     bool bf = false, bx = false, by = false;
