@@ -1157,7 +1157,9 @@ __global__ void k_gauss_rows(const T* __restrict__ x, T* __restrict__ y, int W, 
 // X(id, swizzle, group threads, elements per thread, n, radices...)
 #define ILS_ROW_SPECS(X) X(0, 1, 32, 16, 256, 16, 16) X(1, 3, 32, 32, 960, 32, 30) X(2, 1, 128, 16, 1920, 16, 15, 8) X(3, 1, 256, 16, 3840, 16, 16, 15) X(4, 1, 32, 16, 512, 16, 8, 4)
 // row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
+#ifndef ILS_ROW_SPEC_WIDE  // (tuning override: which row specs use 8-column stencil strips)
 #define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)
+#endif
 #define ILS_COL_SPECS(X) X(0, 1, 32, 16, 512, 16, 8, 4) X(1, 0, 128, 16, 1080, 9, 12, 10) X(2, 1, 256, 16, 2160, 16, 15, 9) X(3, 1, 32, 16, 256, 16, 16) X(4, 1, 128, 16, 720, 16, 9, 5) X(5, 1, 256, 24, 4320, 24, 18, 10)
 
 template <int ID>
