@@ -336,3 +336,36 @@ def test_slab_pipeline_nccl_one_rank_bitwise():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_concurrent_lanes_bitwise_match_single_stream():
+    # the bench's two-lane pattern (one plan, two workspaces, two streams, passes
+    # launched with programmatic dependent launch): every frame bit-identical
+    # to smoothing it alone, over repeated runs (a race would show as a flip)
+    import ctypes as C
+
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0, iters=4)
+    H, W, CH, F = 1080, 1920, 3, 6
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    f = torch.rand((F * CH, H, W), generator=gen, device="cuda")
+    ref = torch.stack([ils.smooth_batch(f[k * CH:(k + 1) * CH], params) for k in range(F)]).reshape(F * CH, H, W)
+    plan = rt.get_plan(CH, H, W, params.c_params(), _lib.ILS_F32, 0)
+    L = _lib.lib()
+    lanes = [torch.cuda.Stream(), torch.cuda.Stream()]
+    wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda") for _ in lanes]
+    sts = [torch.empty(1, dtype=torch.int32, device="cuda") for _ in lanes]
+    for _ in range(3):
+        u = torch.empty_like(f)
+        torch.cuda.synchronize()
+        for k in range(F):
+            ln = k % 2
+            off = k * CH * H * W * 4
+            _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f.data_ptr() + off), C.c_void_p(u.data_ptr() + off), H * W,
+                                    C.c_void_p(wss[ln].data_ptr()), C.c_void_p(lanes[ln].cuda_stream),
+                                    C.c_void_p(sts[ln].data_ptr()), None), "ils_smooth")
+        torch.cuda.synchronize()
+        for st in sts:
+            assert int(st.item()) == _lib.STATUS_CLEAN
+        assert torch.equal(u, ref)
