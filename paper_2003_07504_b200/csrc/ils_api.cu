@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -279,6 +280,7 @@ struct ils_plan {
   int Hl = 0, Wcl = 0;  // local rows, local spectrum columns
   // penalty-splitting baseline (ils_hqs_plan_create): beta_n = beta0 kappa^n
   double hqs_beta0 = 0, hqs_kappa = 0;
+  uint64_t uid = 0;  // process-unique plan id (host-pipeline graph cache key)
 };
 
 namespace {
@@ -765,6 +767,8 @@ ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32
   p->prm = *params;
   p->hqs_beta0 = hqs_beta0;
   p->hqs_kappa = hqs_kappa;
+  static std::atomic<uint64_t> next_uid{1};
+  p->uid = next_uid++;
   const size_t elt = dtype == ILS_F32 ? sizeof(cx<float>) : sizeof(cx<double>);
   const int maxe = dtype == ILS_F32 ? 16 : 8;
   if (device >= 0) {
@@ -1019,11 +1023,25 @@ namespace {
 // setup, serialised in front of every batch group).  Thread-local, so plans
 // stay shareable across threads; intentionally never freed (process exit
 // may run after the CUDA context is gone).
+// Each I/O slot's batch (status reset, the passes) is captured once per
+// (plan, buffers) into a CUDA graph and replayed on its lane: graph launches
+// keep the passes' programmatic-dependent-launch edges inside one submission
+// (ILS_HOST_GRAPHS=0: plain stream launches).
+struct SlotGraphs {
+  uint64_t uid = 0;
+  int kind = -1, ch = 0;
+  const void *io = nullptr, *ws = nullptr;
+  cudaGraphExec_t ex[kIoSlots] = {};
+};
+constexpr int kGraphCache = 8;
+
 struct HostRes {
-  cudaStream_t h2d = nullptr, d2h = nullptr, lane1 = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr, lane1 = nullptr, cap = nullptr;
   cudaEvent_t ev_in[kIoSlots] = {}, ev_comp[kIoSlots] = {}, ev_out[kIoSlots] = {};
   int32_t* hstat = nullptr;
   int hcap = 0;
+  SlotGraphs graphs[kGraphCache];
+  int next_victim = 0;
 };
 
 cudaError_t host_res(int device, int nstat, HostRes** out) {
@@ -1035,6 +1053,7 @@ cudaError_t host_res(int device, int nstat, HostRes** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&n->h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&n->d2h, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&n->lane1, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&n->cap, cudaStreamNonBlocking);
     for (int i = 0; i < kIoSlots && e == cudaSuccess; ++i) {
       e = cudaEventCreateWithFlags(&n->ev_in[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&n->ev_comp[i], cudaEventDisableTiming);
@@ -1065,7 +1084,8 @@ cudaError_t host_res(int device, int nstat, HostRes** out) {
 // run(f_dev, u_dev, status_dev, ws, stream) enqueues one batch.
 template <class Run>
 ils_status host_pipeline(const ils_plan* p, const void* f_host, void* u_host, size_t in_bytes, size_t out_bytes,
-                         int32_t nbatches, void* ws, void* io_dev, void* stream, int32_t* bad_iter, Run run) {
+                         int32_t nbatches, void* ws, void* io_dev, void* stream, int32_t* bad_iter, int kind, int ch,
+                         Run run) {
   if (bad_iter) *bad_iter = -1;
   const size_t slot_in = (in_bytes + 255) & ~size_t(255), slot_out = (out_bytes + 255) & ~size_t(255);
   char* io = static_cast<char*>(io_dev);
@@ -1101,6 +1121,41 @@ ils_status host_pipeline(const ils_plan* p, const void* f_host, void* u_host, si
   cudaEvent_t *ev_in = R->ev_in, *ev_comp = R->ev_comp, *ev_out = R->ev_out;
   int32_t* hstat = R->hstat;
   auto cleanup = [] {};
+  // slot graphs for this (plan, path, buffers): look up, or capture once
+  SlotGraphs* G = nullptr;
+  if (env_int("ILS_HOST_GRAPHS", 1)) {
+    for (SlotGraphs& g : R->graphs)
+      if (g.uid == p->uid && g.kind == kind && g.ch == ch && g.io == io_dev && g.ws == ws) G = &g;
+    if (!G) {
+      G = &R->graphs[R->next_victim];
+      R->next_victim = (R->next_victim + 1) % kGraphCache;
+      for (cudaGraphExec_t& x : G->ex)
+        if (x) {
+          cudaGraphExecDestroy(x);
+          x = nullptr;
+        }
+      G->uid = 0;
+      for (int sl = 0; sl < NS; ++sl) {
+        ILS_TRY(cudaStreamBeginCapture(R->cap, cudaStreamCaptureModeThreadLocal));
+        const ils_status r = run(fslot[sl], uslot[sl], st[sl], wsl[sl & 1], R->cap);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(R->cap, &graph);
+        if (r != ILS_OK) {
+          if (graph) cudaGraphDestroy(graph);
+          return r;
+        }
+        if (ec != cudaSuccess) return fail(ILS_ECUDA, "host pipeline capture: %s", cudaGetErrorString(ec));
+        const cudaError_t ei = cudaGraphInstantiate(&G->ex[sl], graph, 0);
+        cudaGraphDestroy(graph);
+        if (ei != cudaSuccess) return fail(ILS_ECUDA, "host pipeline graph: %s", cudaGetErrorString(ei));
+      }
+      G->uid = p->uid;
+      G->kind = kind;
+      G->ch = ch;
+      G->io = io_dev;
+      G->ws = ws;
+    }
+  }
   // the caller's stream may still be producing host-visible state: order h2d after it
   ILS_TRY(cudaEventRecord(ev_out[0], s));
   ILS_TRY(cudaStreamWaitEvent(h2d, ev_out[0], 0));
@@ -1115,10 +1170,14 @@ ils_status host_pipeline(const ils_plan* p, const void* f_host, void* u_host, si
     ILS_TRY(cudaEventRecord(ev_in[sl], h2d));
     ILS_TRY(cudaStreamWaitEvent(lane[ln], ev_in[sl], 0));
     if (k >= NS) ILS_TRY(cudaStreamWaitEvent(lane[ln], ev_out[sl], 0));  // u slot drained by batch k-NS
-    ils_status r = run(fslot[sl], uslot[sl], st[sl], wsl[ln], lane[ln]);
-    if (r != ILS_OK) {
-      cleanup();
-      return r;
+    if (G) {
+      ILS_TRY(cudaGraphLaunch(G->ex[sl], lane[ln]));  // = run(fslot[sl], uslot[sl], st[sl], wsl[ln], lane[ln])
+    } else {
+      ils_status r = run(fslot[sl], uslot[sl], st[sl], wsl[ln], lane[ln]);
+      if (r != ILS_OK) {
+        cleanup();
+        return r;
+      }
     }
     ILS_TRY(cudaEventRecord(ev_comp[sl], lane[ln]));
     ILS_TRY(cudaStreamWaitEvent(d2h, ev_comp[sl], 0));
@@ -1152,7 +1211,7 @@ ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, 
   if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
   if (ps != (int64_t)p->H * p->W) return fail(ILS_EINVAL, "host planes must be dense (plane_stride == H*W)");
   const size_t bytes = (size_t)p->B * ps * (p->dtype == ILS_F32 ? 4 : 8);
-  return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter,
+  return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter, 0, 0,
                        [&](void* fd, void* ud, int32_t* st, void* w, cudaStream_t ls) {
                          return ils_smooth(p, fd, ud, ps, w, ls, st, nullptr);
                        });
@@ -1164,7 +1223,7 @@ ils_status ils_smooth_host_u8(const ils_plan* p, const uint8_t* f_host, uint8_t*
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
   const size_t bytes = (size_t)p->B * p->H * p->W;
-  return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter,
+  return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter, 1, channels,
                        [&](void* fd, void* ud, int32_t* st, void* w, cudaStream_t ls) {
                          return ils_smooth_u8(p, static_cast<const uint8_t*>(fd), static_cast<uint8_t*>(ud), channels,
                                               w, ls, st);
