@@ -328,7 +328,15 @@ def smooth_color(planes, spec, lam, iters=4, c=None, luminance_only=False, trace
         ys = res[0] if trace else res
         out = list(yuv_to_rgb(ys, cu, cv))
         return (out, res[1]) if trace else out
-    results = [smooth_plane(p, spec, lam, iters, c, trace, workers) for p in planes]
+    if workers > 1 and len(planes) > 1:
+        # smoother.py:203-212: per-channel smooths on a thread pool of <= 3
+        # (numpy / scipy.fft release the GIL), each with the same `workers`
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=min(3, len(planes), workers)) as pool:
+            results = list(pool.map(lambda p: smooth_plane(p, spec, lam, iters, c, trace, workers), planes))
+    else:
+        results = [smooth_plane(p, spec, lam, iters, c, trace, workers) for p in planes]
     if trace:
         outs = [r[0] for r in results]
         summed = [float(sum(v)) for v in zip(*(r[1] for r in results))]
