@@ -612,12 +612,23 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
     a.fcopy = reinterpret_cast<T*>(static_cast<char*>(ws) + p->off_fcopy);
     a.f = a.fcopy;
     a.f_ps = (int64_t)p->H * p->W;
-    const int npx = p->H * p->W;
-    const int frames = p->B / ch;
-    const long long work = (ch == 3 && (npx & 3) == 0) ? npx / 4 : (long long)npx * ch;  // per frame
-    const int bx = (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, (long long)p->sms * 8 / frames));
-    k_u8_planar<T><<<dim3(bx, frames), 256, 0, s>>>(f8, a.fcopy, ch, npx);
-    ILS_CUDA(cudaGetLastError());
+    // compile-time fp32 plans with 3-channel rows: the first row pass loads the
+    // interleaved byte rows itself (TMA into the tail of each line slot) and
+    // writes the planar f on the way; otherwise a separate deinterleave kernel
+    const bool fuse = std::is_same<T, float>::value && p->row_spec >= 0 && p->packed && p->W % 128 == 0 &&
+                      ch == 3 && (size_t)p->LP * sizeof(cx<T>) >= (size_t)p->W * (ch + 1) &&
+                      !env_int("ILS_NO_FUSED_INGEST", 0);
+    if (fuse) {
+      a.f8 = f8;
+    } else {
+      const int npx = p->H * p->W;
+      const int frames = p->B / ch;
+      const long long work = (ch == 3 && (npx & 3) == 0) ? npx / 4 : (long long)npx * ch;  // per frame
+      const int bx =
+          (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, (long long)p->sms * 8 / frames));
+      k_u8_planar<T><<<dim3(bx, frames), 256, 0, s>>>(f8, a.fcopy, ch, npx);
+      ILS_CUDA(cudaGetLastError());
+    }
   }
   const int iters = p->prm.iters;
   cx<T>* cur = Sa;

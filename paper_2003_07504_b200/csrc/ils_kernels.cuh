@@ -480,6 +480,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   // specialised fp32 final pass (no trace, no 8-bit egress): each line group
   // checks and stores its own row as soon as its transform is done
   constexpr bool FINLINE8 = SMODE == kU8Modes + MODE_FIN && BULK && sizeof(T) == 4;  // same, 8-bit egress
+  // 8-bit ingest fused into the first pass: each line's interleaved byte row
+  // arrives by TMA in the tail of its line slot and is widened in place
+  constexpr bool INGEST8 = SMODE == kU8Modes + MODE_F0 && BULK && sizeof(T) == 4;
   constexpr bool FINLINE = (SMODE == MODE_FIN && BULK && sizeof(T) == 4) || FINLINE8;
   constexpr bool SOFTOK = SMODE < 0 || U8;  // kernels that accept the soft-threshold penalty
   const int MODE = U8 ? SMODE - kU8Modes : (SMODE >= 0 ? SMODE : A.mode);  // block-uniform
@@ -573,7 +576,13 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         {
           const int i = tid;
           const int y = A.wrap ? wrapi(y0 + i, H) : y0 + i;
-          if (MODE == MODE_F0) {
+          if (INGEST8) {
+            const unsigned bytes = (unsigned)(W * A.ch);
+            const unsigned char* src = A.f8 + ((size_t)(b / A.ch) * H + y) * (size_t)W * A.ch;
+            unsigned char* dst = reinterpret_cast<unsigned char*>(L.line(i)) + (size_t)A.LP * sizeof(cx<T>) - bytes;
+            mbar_expect_tx(&bars[i], bytes);
+            bulk_g2s(dst, src, bytes, &bars[i]);
+          } else if (MODE == MODE_F0) {
             const unsigned bytes = (unsigned)(W * sizeof(T));
             mbar_expect_tx(&bars[i], bytes);
             bulk_g2s(L.line(i), fpl + (size_t)y * A.f_rp, bytes, &bars[i]);
@@ -625,7 +634,41 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
         cp_async_wait_keep(mine - 1 - li);
         g.sync();
       }
-      if (MODE == MODE_F0) {
+      if constexpr (INGEST8) {
+        // widen channel b % C of the byte row (3 bytes per pixel, 4 pixels per
+        // lane and round) to v / 255 floats at the front of the slot, and
+        // write the band's own rows to the planar f the later passes add.
+        // Rounds go front to back: round k's float stores end below round
+        // k+1's byte loads (the host only fuses when the slot's byte tail
+        // starts at >= W bytes), so one warp barrier per round suffices.
+        const int C = A.ch, c = b % C;
+        const unsigned char* src8 =
+            reinterpret_cast<const unsigned char*>(z) + (size_t)A.LP * sizeof(cx<T>) - (size_t)W * C;
+        float* zf = reinterpret_cast<float*>(z);
+        T* fc = (i >= 1 && i <= nb) ? A.fcopy + (size_t)b * A.f_ps + (size_t)(y0 + i) * A.f_rp : nullptr;
+        for (int q0 = 0; q0 < W / 4; q0 += g.size()) {
+          const int q = q0 + g.rank;
+          unsigned wd[3] = {0u, 0u, 0u};
+          if (q < W / 4) {
+            const unsigned* w = reinterpret_cast<const unsigned*>(src8 + 12 * q);
+            wd[0] = w[0];
+            wd[1] = w[1];
+            wd[2] = w[2];
+          }
+          g.sync();
+          if (q < W / 4) {
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int pos = 3 * k + c;  // byte of pixel k, channel c (C == 3)
+              v[k] = u8_to((wd[pos >> 2] >> (8 * (pos & 3))) & 0xffu, T{});
+            }
+            const float4 o = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4*>(zf + 4 * q) = o;
+            if (fc) *reinterpret_cast<float4*>(fc + 4 * q) = o;
+          }
+        }
+      } else if (MODE == MODE_F0) {
         if (!PACKED)
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
@@ -1229,6 +1272,7 @@ cudaError_t launch_row_impl(const RowArgs<T>& a, dim3 grid, int threads, size_t 
   auto k = k_row<T, PACKED, FS, WIDE, -1>;
   if (a.f8 || a.u8) {
     if (a.epart) return cudaErrorInvalidValue;  // no energy trace on the 8-bit path
+    if (a.mode == MODE_F0 && a.f8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_F0>;
     if (a.mode == MODE_FIN && a.u8) k = k_row<T, PACKED, FS, WIDE, kU8Modes + MODE_FIN>;
   } else if (a.epart == nullptr && (a.pen.kind != 2 || a.mode == MODE_FIN)) {
     if (a.mode == MODE_F0) k = k_row<T, PACKED, FS, WIDE, MODE_F0>;
