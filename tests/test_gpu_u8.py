@@ -83,3 +83,16 @@ def test_u8_rejects_bad_frames():
 
     with pytest.raises(ValueError):
         ils.smooth_frames_u8(np.zeros((8, 8, 3), dtype=np.uint8), replace(prm, color_mode=ils.ColorMode.LUMINANCE_ONLY))
+
+
+def test_fused_ingest_equals_planar_path_1080p():
+    # 1080p RGB frames take the fused 8-bit ingest (TMA byte rows widened in the
+    # first row pass); it must equal smoothing the v/255 planes and quantising
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0)
+    rng = np.random.default_rng(9)
+    f8 = torch.from_numpy(rng.integers(0, 256, (2, 1080, 1920, 3), dtype=np.uint8)).cuda()
+    got = ils.smooth_frames_u8(f8, params)
+    planes = (f8.permute(0, 3, 1, 2).reshape(6, 1080, 1920).to(torch.float64) / 255.0).to(torch.float32)
+    u = ils.smooth_batch(planes, params)
+    want = torch.floor(torch.clamp(u, 0, 1) * 255 + 0.5).to(torch.uint8).reshape(2, 3, 1080, 1920).permute(0, 2, 3, 1)
+    assert torch.equal(got, want)
