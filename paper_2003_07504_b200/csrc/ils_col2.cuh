@@ -57,7 +57,9 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
   const bool actA = r < N2;  // stages A and C: r = n2
 
   // ---------------- stage A: strided rows -> DFT_N1 -> twiddle -> smem
+#ifndef ILS_PDL_LATE
   pdl_trigger();
+#endif
   for (int m = t; m < H; m += S::NT) {  // constant tables: before the wait on the previous pass
     stw[m] = ldg_cx(A.tw2 + m);
     swy[m] = __ldg(A.wy + m);
@@ -98,6 +100,9 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
   }
   __syncthreads();
 
+#ifdef ILS_PDL_LATE
+  pdl_trigger();
+#endif
   // ---------------- stage C: inverse DFT_N1 -> rows
   if (actA) {
     const cx<float>* d = buf + r * CW + c;

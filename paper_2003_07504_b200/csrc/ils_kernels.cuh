@@ -518,7 +518,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   TwCache<T, FS> twc;
   fill_twcache(twc, A.fft, g);
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
+#ifndef ILS_PDL_LATE
   pdl_trigger();
+#endif
   if (MODE == MODE_IT && tid < nb && (W * sizeof(T)) % 16 == 0 && (A.f_rp * sizeof(T)) % 16 == 0) {
     // the stencil reads f one row at a time: pull the band's rows into L2 now
     // (f is the call's input, written before the first pass: no need to wait
@@ -939,6 +941,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     }
   }
 
+#ifdef ILS_PDL_LATE  // (tuning: let the next pass launch only once this one reaches its last phase)
+  pdl_trigger();
+#endif
   // ---------------- phase C: r2c of rhs rows -> S_out (group per line)
   for (int i = g.id; i < nb; i += ngroups) {
     cx<T>* z = L.line(i);
