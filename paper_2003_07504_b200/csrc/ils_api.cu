@@ -322,7 +322,8 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   // packing twiddles staged in shared memory, except for kind-3 plans (L1)
   const size_t wreal_bytes = (p.packed && p.rowf.swz != 3) ? (size_t)(p.N / 2 + 1) * elt : 0;
   // Band size: minimise (waves x per-CTA work).  A CTA of band b transforms
-  // b+2 lines c2r and b lines r2c; 2 CTAs fit an SM while smem <= ~113 KB.
+  // b+2 lines c2r and b lines r2c; k CTAs fit an SM while smem <= 228/k KB
+  // and the register budget (kRowBlocksOf) allows them.
   const int force = env_int("ILS_ROW_BAND", 0);
   double best = 1e300;
   for (int band = 1; band <= std::min(p.H, kMaxBandLines - 2); ++band) {

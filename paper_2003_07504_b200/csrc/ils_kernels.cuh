@@ -414,11 +414,11 @@ constexpr bool kBulkRows = sizeof(T) == 4 && FS::n > 0 && (2 * FS::n) % 8 == 0;
 // SMODE >= 0: kernel specialised for that mode without trace (the hot
 // kernels; dead phases compiled out keeps the code inside the I-cache);
 // SMODE = -1: any mode from A.mode, optional energy trace.
-// register budget: 3 CTAs / SM for plans with <= 16 elements per thread, else 2
-// compile-time plans budget registers for 3 resident CTAs per SM (80 for
+// Register budget: compile-time plans budget for 3 resident CTAs per SM (80 for
 // the 32 x 30 plan, no spills): with a band of 6 the row pass then leaves
 // room on every SM for the other lane's column-pass CTAs, which is worth more
-// than the band-12 CTA's lower halo overhead (4993 -> 5859 frames/s)
+// than the band-12 CTA's lower halo overhead (4993 -> 5859 frames/s);
+// runtime plans for 2
 #ifndef ILS_ROW_MINB  // (tuning override: resident row CTAs per SM the registers are budgeted for)
 template <class FS>
 constexpr int kRowBlocksOf = FS::n > 0 ? 3 : 2;
