@@ -38,7 +38,7 @@ typedef enum {
   ILS_ENONFINITE_INPUT = 2, /* non-finite input plane -> ValueError (image.py:43-44) */
   ILS_ENONFINITE = 3,       /* non-finite iterate -> NumericalError (smoother.py:166-167) */
   ILS_ECUDA = 4,            /* CUDA runtime failure */
-  ILS_EUNSUPPORTED = 5      /* a side has a prime factor > 61 -> ValueError */
+  ILS_EUNSUPPORTED = 5      /* a side has a prime factor > 4096 (fp32) / 2048 (fp64) -> ValueError */
 } ils_status;
 
 typedef enum { ILS_CHARBONNIER = 0, ILS_WELSCH = 1, ILS_SOFT = 2 /* HQS plans only */ } ils_penalty_kind;

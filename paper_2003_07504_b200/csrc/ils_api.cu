@@ -55,6 +55,9 @@ const int kUnrolled[] = {16, 15, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2};
 // (generic primes: one butterfly per thread).
 bool pass_fits(int R, long long n, int G, int maxe, bool unrolled = false) {
   const long long tasks = n / R;
+  // generic primes beyond one butterfly per thread: fft_pass_bigprime, one
+  // output per register slot (the device dispatch in fft_line_rt mirrors this)
+  if (R > 16 && !unrolled && (R > kMaxGenericPrime || tasks > G)) return n <= (long long)maxe * G;
   const int km = (R <= 16 || unrolled) ? std::max(1, maxe / R) : 1;  // KmOf<R, ME> (ils_fft.cuh)
   return (tasks + G - 1) / G <= km;
 }
@@ -84,18 +87,22 @@ void dfs(int rem, int maxr, long long elems, int nthr, int maxe, std::vector<int
     return;
   }
   if (found && cur.size() + 1 > best.size()) return;
-  // generic odd primes 17..61 must stand alone
-  for (int p = 17; p <= kMaxGenericPrime; p += 2) {
-    bool prime = true;
-    for (int d = 3; d * d <= p; d += 2)
-      if (p % d == 0) prime = false;
-    if (prime && rem % p == 0) {
-      if (p > maxr || !pass_fits(p, elems, nthr, maxe)) return;
-      cur.push_back(p);
-      dfs(rem / p, p, elems, nthr, maxe, cur, best, found);
-      cur.pop_back();
-      return;
+  // generic odd primes (17 and up) must stand alone, largest first (radices
+  // are placed in non-increasing order)
+  int big = 1;
+  for (int d = 2, r = rem; d <= r; ++d) {
+    if ((long long)d * d > r) d = r;
+    while (r % d == 0) {
+      r /= d;
+      big = d;
     }
+  }
+  if (big >= 17) {
+    if (big > maxr || !pass_fits(big, elems, nthr, maxe)) return;
+    cur.push_back(big);
+    dfs(rem / big, big, elems, nthr, maxe, cur, best, found);
+    cur.pop_back();
+    return;
   }
   for (int R : kUnrolled) {
     if (R > maxr || rem % R) continue;
@@ -106,10 +113,13 @@ void dfs(int rem, int maxr, long long elems, int nthr, int maxe, std::vector<int
   }
 }
 
-bool has_big_prime(int n) {
+// fft_pass_bigprime holds MAXE outputs per thread of a group of <= 256: a
+// line whose largest prime factor exceeds that cannot be planned
+constexpr int kMaxBigPrimeLine = 16 * 256;
+bool has_big_prime(int n, int dtype) {
   for (int p = 2; (long long)p * p <= n; ++p)
     while (n % p == 0) n /= p;
-  return n > kMaxGenericPrime;
+  return n > kMaxBigPrimeLine / (dtype == ILS_F32 ? 1 : 2);
 }
 
 struct SpecHost {
@@ -763,9 +773,9 @@ ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32
   if (batch < 1) return fail(ILS_EINVAL, "batch must be >= 1, got %d", batch);
   if (height < 1 || width < 1) return fail(ILS_EINVAL, "invalid plan size %dx%d", height, width);
   if (dtype != ILS_F32 && dtype != ILS_F64) return fail(ILS_EINVAL, "unknown dtype %d", dtype);
-  if (has_big_prime(height) || has_big_prime(width % 2 == 0 ? width / 2 : width))
-    return fail(ILS_EUNSUPPORTED, "plane size %dx%d has a prime factor > %d (unsupported FFT length)", height, width,
-                kMaxGenericPrime);
+  if (has_big_prime(height, dtype) || has_big_prime(width % 2 == 0 ? width / 2 : width, dtype))
+    return fail(ILS_EUNSUPPORTED, "plane size %dx%d has a prime factor beyond the direct-DFT pass (%d)", height,
+                width, kMaxBigPrimeLine / (dtype == ILS_F32 ? 1 : 2));
   ils_plan* p = new ils_plan();
   p->B = batch;
   p->H = height;

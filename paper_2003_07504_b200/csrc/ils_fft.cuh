@@ -26,8 +26,8 @@
 //
 // Twiddles: one table entry w_{Ns R}^m per butterfly class, computed on the
 // host in double with exact integer angle reduction; powers in registers.
-// Radices 2..16 are unrolled; odd primes 17..61 use a looped direct DFT
-// (generic sizes only).
+// Radices 2..16 are unrolled; odd primes 17..61 use a looped direct DFT per
+// butterfly, larger primes a direct DFT per output (generic sizes only).
 #pragma once
 
 #include "ils_dft.cuh"
@@ -269,6 +269,51 @@ __device__ __noinline__ void fft_pass_generic(cx<T>* __restrict__ x, int n, int 
   g.sync();
 }
 
+// Large prime R (> 61, or a 17..61 prime with more butterflies than group
+// threads): outputs are spread over the group instead of butterflies, so
+// register need is MAXE accumulators whatever R is (the line must satisfy
+// n <= MAXE * G).  Output slot o = (j - m) R + m + k Ns of butterfly j
+// (m = j mod Ns) is the direct R-point sum over that butterfly's twiddled
+// inputs, O(R) per output -- the reference (scipy.fft, solver.py:24-30)
+// accepts every length, and these lengths are correctness cases, not hot.
+template <typename T, int DIR, int MAXE, class Grp, class Lay>
+__device__ __noinline__ void fft_pass_bigprime(cx<T>* __restrict__ x, int n, int Ns, int R,
+                                               const cx<T>* __restrict__ tw, const cx<T>* __restrict__ wr,
+                                               const Grp g, const Lay lay_in, const Lay lay_out) {
+  const int nb = n / R;
+  cx<T> acc[MAXE];
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) {
+    const int o = g.rank + i * g.size();
+    acc[i] = cx<T>{T(0), T(0)};
+    if (o < n) {
+      const int m = o % Ns, q = o / Ns;
+      const int k = q % R, j = (q / R) * Ns + m;
+      int e = 0;  // r k mod R
+      for (int r = 0; r < R; ++r) {
+        cx<T> a = x[lay_in(j + r * nb)];
+        if (Ns > 1 && r > 0) {
+          cx<T> ww = ldg_cx(tw + m * (R - 1) + r - 1);
+          if (DIR > 0) ww.y = -ww.y;
+          a = cmul(a, ww);
+        }
+        cx<T> w = ldg_cx(wr + e);
+        if (DIR > 0) w.y = -w.y;
+        acc[i] = acc[i] + cmul(a, w);
+        e += k;
+        if (e >= R) e -= R;
+      }
+    }
+  }
+  g.sync();
+#pragma unroll
+  for (int i = 0; i < MAXE; ++i) {
+    const int o = g.rank + i * g.size();
+    if (o < n) x[lay_out(o)] = acc[i];
+  }
+  g.sync();
+}
+
 // Runtime-planned path (any supported n): each radix pass is its own
 // non-inlined function so the register allocator sees one radix at a time
 // (inlining all cases into one body blows up live ranges and spills).
@@ -307,7 +352,11 @@ __device__ __forceinline__ void fft_line_rt(cx<T>* __restrict__ x, const FftDev<
       ILS_FFT_CASE(16)
 #undef ILS_FFT_CASE
       default:
-        fft_pass_generic<T, DIR>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g, lay_in, lay_out);
+        if (R <= kMaxGenericPrime && nb <= g.size())
+          fft_pass_generic<T, DIR>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g, lay_in, lay_out);
+        else
+          fft_pass_bigprime<T, DIR, MaxElems<T>::value>(x, P.n, Ns, R, tw, P.tw + P.gen_off[p], g, lay_in,
+                                                        lay_out);
         break;
     }
     Ns *= R;

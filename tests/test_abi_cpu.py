@@ -119,8 +119,20 @@ def test_u8_ingest_newton_division_is_exact():
 
 def test_unsupported_prime_and_bad_params_map_to_valueerror():
     prm = ils.SmoothParams(ils.Charbonnier(0.8), 1.0).c_params()
-    st, _ = _host_plan(1, 1031, 64, prm)
+    # primes > 61 plan onto the direct-DFT pass, up to one output per register
+    # slot of a 256-thread group (16 fp32 / 8 fp64 per thread)
+    for h, w, dt in [(1031, 64, _lib.ILS_F32), (97, 1, _lib.ILS_F32), (1919, 2 * 1009, _lib.ILS_F32),
+                     (2039, 6, _lib.ILS_F64), (4093, 64, _lib.ILS_F32)]:
+        st, p = _host_plan(1, h, w, prm, dt)
+        assert st == 0, (h, w, dt)
+        info = _lib.PlanInfo()
+        assert _lib.lib().ils_plan_get_info(p, C.byref(info)) == 0
+        assert max(info.col_radix) == max(q for q in range(2, h + 1) if h % q == 0 and
+                                          all(q % d for d in range(2, q)))
+        _lib.lib().ils_plan_destroy(p)
+    st, _ = _host_plan(1, 4099, 64, prm)
     assert st == _lib.ILS_EUNSUPPORTED
+    assert _host_plan(1, 2053, 64, prm, _lib.ILS_F64)[0] == _lib.ILS_EUNSUPPORTED
     with pytest.raises(ValueError, match="prime factor"):
         _lib.check(st)
     bad = _lib.Params(_lib.ILS_CHARBONNIER, 1.5, 1e-4, 0.0, 1.0, 300.0, 4)
