@@ -201,7 +201,7 @@ double bank_cost(int n, const std::vector<int>& radix, int G, int kind, int E, i
 // (fp32 hot sizes) fixes radices, group size and layout; otherwise the plan
 // with fewest passes at the smallest group size G (32..256) for which every
 // pass fits, and the layout with fewer simulated bank conflicts.
-bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
+bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E, int maxG = 256) {
   out = FftHost{};
   out.n = n;
   if (spec) {
@@ -212,7 +212,7 @@ bool make_fft(int n, int maxe, FftHost& out, const SpecHost* spec, int E) {
     out.swz = spec->swz;
   } else {
     bool ok = n <= 1;
-    for (int G = 32; G <= 256 && !ok; G *= 2) {
+    for (int G = 32; G <= maxG && !ok; G *= 2) {
       std::vector<int> cur, best;
       bool found = false;
       dfs(n, 1 << 30, n, G, maxe, cur, best, found);
@@ -273,6 +273,7 @@ struct ils_plan {
   int band, row_threads, row_grid, LP;
   size_t row_smem;
   int C, CS, col_threads, col_grid;
+  bool col_wide = false;  // k_col<FftRtWide>: 512 threads, one group per line
   size_t col_smem;
   int row_spec = -1, col_spec = -1;  // compile-time FFT plan ids (-1: runtime plan)
   int col2 = -1;                     // two-stage column solve (ILS_COL2_SPECS id), -1: k_col
@@ -368,12 +369,18 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
 bool choose_col(ils_plan& p, int maxe, size_t elt) {
   const SpecHost* spec = p.dtype == ILS_F32 ? find_spec(kColSpecs, p.H) : nullptr;
   p.col_spec = spec ? spec->id : -1;
+  p.col_wide = false;
   if (!make_fft(p.H, maxe, p.colf, spec, elt == 8 ? 16 : 8)) {
-    if (!spec || !make_fft(p.H, maxe, p.colf, nullptr, elt == 8 ? 16 : 8)) return false;
     p.col_spec = -1;
+    if (!make_fft(p.H, maxe, p.colf, nullptr, elt == 8 ? 16 : 8)) {
+      // long columns: one 512-thread group per line (k_col<FftRtWide>)
+      if (!make_fft(p.H, maxe, p.colf, nullptr, elt == 8 ? 16 : 8, 2 * kColThreads)) return false;
+      p.col_wide = true;
+    }
   }
   const int E = elt == 8 ? 16 : 8;  // complex elements per 128 B
-  const int ngroups = kColThreads / p.colf.G;
+  const int col_nt = p.col_wide ? 2 * kColThreads : kColThreads;
+  const int ngroups = col_nt / p.colf.G;
   const int force = env_int("ILS_COL_COLS", 0);
   const int base = (p.H + E - 1) / E * E;
   double best = 1e300;
@@ -402,7 +409,7 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
     const size_t smem = (size_t)C * bestCS * elt + (size_t)p.H * (elt / 2);  // tile + wy
     if (smem > 227 * 1024) break;
     // resident CTAs/SM: k_col is register-bounded to 3 (launch bounds), smem to 228 KB
-    const int per_sm = (int)std::min<size_t>(kColMinBlocks, (228 * 1024) / (smem + 1024));
+    const int per_sm = (int)std::min<size_t>(p.col_wide ? 1 : kColMinBlocks, (228 * 1024) / (smem + 1024));
     const long strips = (p.Wc + C - 1) / C;
     const long ctas = (long)p.B * strips;
     // the pass is issue-bound: time ~ the busiest SM's column count
@@ -424,7 +431,7 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
     }
   }
   if (best == 1e300) return false;
-  p.col_threads = kColThreads;
+  p.col_threads = col_nt;
   p.col_grid = (p.Wc + p.C - 1) / p.C;
   // the solve pass (COL_SOLVE) of fp32 plans whose height has a two-stage
   // kernel runs k_col2; the standalone transforms keep k_col
@@ -594,6 +601,7 @@ cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
         break;
     }
   }
+  if (p->col_wide) return launch_col_impl<T, FftRtWide>(a, grid, p->col_threads, p->col_smem, s);
   return launch_col_impl<T, FftRt>(a, grid, p->col_threads, p->col_smem, s);
 }
 
@@ -1529,7 +1537,8 @@ ils_status slab_col_t(const ils_plan* p, cx<T>* recv, cx<T>* send, cudaStream_t 
         break;
     }
   }
-  e = launch_col_impl<T, FftRt>(c, grid, p->col_threads, p->col_smem, s);
+  e = p->col_wide ? launch_col_impl<T, FftRtWide>(c, grid, p->col_threads, p->col_smem, s)
+                  : launch_col_impl<T, FftRt>(c, grid, p->col_threads, p->col_smem, s);
   if (e != cudaSuccess) return fail(ILS_ECUDA, "slab col pass: %s", cudaGetErrorString(e));
   return ILS_OK;
 }

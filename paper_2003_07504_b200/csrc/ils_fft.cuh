@@ -380,6 +380,10 @@ struct FftRt {
   static constexpr int ME = 1;  // no twiddle cache for runtime plans
   static constexpr int npass = 0;
 };
+// FftRtWide: a runtime plan whose column lines need a 512-thread group
+// (H > 4096 fp32 / 2048 fp64 elements at <= MAXE per thread): k_col runs it
+// with 512 threads and a 1-CTA/SM register budget
+struct FftRtWide : FftRt {};
 template <int SWZ, int GG, int ME_, int N, int... Rs>
 struct FftCt {
   static constexpr int n = N;

@@ -23,6 +23,8 @@ template cudaError_t launch_row_impl<ILS_INST_ROW_RT, true, FftRt, true>(const R
 #ifdef ILS_INST_COL_RT
 template cudaError_t launch_col_impl<ILS_INST_COL_RT, FftRt>(const ColArgs<ILS_INST_COL_RT>&, dim3, int, size_t,
                                                              cudaStream_t);
+template cudaError_t launch_col_impl<ILS_INST_COL_RT, FftRtWide>(const ColArgs<ILS_INST_COL_RT>&, dim3, int, size_t,
+                                                                 cudaStream_t);
 #endif
 #ifdef ILS_INST_ROW_SPEC
 template cudaError_t launch_row_impl<float, true, RowSpec<ILS_INST_ROW_SPEC>::type,

@@ -953,8 +953,10 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
       const AddPair<T> pre{reinterpret_cast<const cx<T>*>(fpl + (size_t)(r0 + i) * A.f_rp)};
       fft_line<T, -1, FS>(z, A.fft, g, pre, &twc);
     } else {
-      if (MODE == MODE_IT)  // unpacked (odd W): add f as its own sweep
+      if (MODE == MODE_IT) {  // unpacked (odd W): add f as its own sweep
         for (int x = g.rank; x < W; x += g.size()) z[x].x += fpl[(size_t)(r0 + i) * A.f_rp + x];
+        g.sync();  // the first pass reads other threads' elements
+      }
       fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
     }
     if (PACKED) r2c_post<T, WSMEM>(z, A.N, swreal, g);
@@ -1006,8 +1008,13 @@ struct UniformScale {
 template <class FS>
 constexpr int kColBlocksOf = FS::ME > 16 ? 2 : kColMinBlocks;
 
+template <class FS>
+constexpr int kColThreadsOf = std::is_same<FS, FftRtWide>::value ? 2 * kColThreads : kColThreads;
+template <class FS>
+constexpr int kColLaunchBlocksOf = std::is_same<FS, FftRtWide>::value ? 1 : kColBlocksOf<FS>;
+
 template <typename T, class FS>
-__global__ void __launch_bounds__(kColThreads, kColBlocksOf<FS>) k_col(const ColArgs<T> A) {
+__global__ void __launch_bounds__(kColThreadsOf<FS>, kColLaunchBlocksOf<FS>) k_col(const ColArgs<T> A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cx<T>* tile = reinterpret_cast<cx<T>*>(smem_raw);
   T* swy = reinterpret_cast<T*>(tile + A.C * A.CS);  // wy[0..H) staged once per CTA

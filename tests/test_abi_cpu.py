@@ -130,6 +130,14 @@ def test_unsupported_prime_and_bad_params_map_to_valueerror():
         assert max(info.col_radix) == max(q for q in range(2, h + 1) if h % q == 0 and
                                           all(q % d for d in range(2, q)))
         _lib.lib().ils_plan_destroy(p)
+    for h, dt, nt in [(5000, _lib.ILS_F32, 512), (8192, _lib.ILS_F32, 512), (4100, _lib.ILS_F64, 512),
+                      (1080, _lib.ILS_F32, 256)]:
+        st, p = _host_plan(1, h, 64, prm, dt)  # long columns: 512-thread k_col groups
+        assert st == 0, (h, dt)
+        info = _lib.PlanInfo()
+        assert _lib.lib().ils_plan_get_info(p, C.byref(info)) == 0
+        assert info.col_threads == nt
+        _lib.lib().ils_plan_destroy(p)
     st, _ = _host_plan(1, 4099, 64, prm)
     assert st == _lib.ILS_EUNSUPPORTED
     assert _host_plan(1, 2053, 64, prm, _lib.ILS_F64)[0] == _lib.ILS_EUNSUPPORTED

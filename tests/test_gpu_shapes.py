@@ -58,3 +58,36 @@ def test_batch_placement_invariance_odd_shapes(shape):
     for i in (0, 3):
         b = ils.smooth_batch(x[i:i + 1].clone(), params)
         assert torch.equal(b[0], a[i])
+
+
+@pytest.mark.parametrize("shape,prec", [((5000, 64), "fp32"), ((8192, 24), "fp32"), ((4100, 96), "fp64"),
+                                        ((4100, 96), "fp32")])
+def test_long_columns_512_thread_groups(shape, prec):
+    # columns longer than a 256-thread group holds run k_col with one
+    # 512-thread group per line (k_col<FftRtWide>)
+    f = np.random.default_rng(77).random(shape)
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0, iters=2)
+    ref = O.smooth_plane(f, O.Charbonnier(0.8, 1e-4), 1.0, 2)
+    u = ils.smooth_plane(f, params, precision=prec)
+    assert np.max(np.abs(u - ref)) <= (1e-4 if prec == "fp32" else 1e-10)
+    x = torch.from_numpy(f[None]).to("cuda", torch.float32 if prec == "fp32" else torch.float64)
+    X = ils._runtime.rfft2_device(x).cpu().numpy()[0]
+    R = np.fft.rfft2(f)
+    assert np.max(np.abs(X - R)) / np.max(np.abs(R)) < (2e-6 if prec == "fp32" else 1e-13)
+
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_odd_width_multiwarp_groups_repeatable(prec):
+    # odd widths run the unpacked row path; at 1919 = 19 * 101 in fp64 one
+    # 256-thread group owns each line, so any missing group barrier in that
+    # path shows up as run-to-run differences (it did: the f-add sweep before
+    # the forward transform)
+    f = np.random.default_rng(5).random((1080, 1919))
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0)
+    x = torch.from_numpy(f[None]).to("cuda", torch.float32 if prec == "fp32" else torch.float64)
+    first = ils.smooth_batch(x, params)
+    for _ in range(8):
+        assert torch.equal(ils.smooth_batch(x, params), first)
+    ref = O.smooth_plane(f, O.Charbonnier(0.8, 1e-4), 1.0, 4)
+    assert np.max(np.abs(first[0].cpu().numpy() - ref)) <= (1e-4 if prec == "fp32" else 1e-10)
