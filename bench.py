@@ -25,8 +25,18 @@ roofline  the dominant kernel (fused row pass, iterations >= 1), CUDA events
           bandwidth in MEASURED_PEAKS.json; `traffic` = ncu DRAM bytes per
           launch (profiles/traffic.json).  `issue`: the bound that binds --
           ncu warp instructions per launch / time vs 4 per SM per cycle.
+e2e_dropin  the reference's own entry point, smooth_color(MultiImage of
+          float64 numpy planes) -> MultiImage of float64 planes
+          (pkg/src/ilsmooth/smoother.py:175-217), one image per call.
+parity    frame 0 of the device run against the float64 oracle
+          (max-abs, PSNR: the north star's 1e-4 / 60 dB).
+c4, c5    BASELINE.json configs[3..4]: 3840x2160 RGB video (256 frames,
+          sharded over ranks, frames/s) and one 7680x4320 RGB image
+          (Welsch, N=10; ms per image; at N > 1 the slab decomposition with
+          the NCCL all-to-all transposes), each with its whole-path roofline
+          fraction and a bitwise check against the 1-GPU result.
 cpu_baseline  the oracle port (numpy/scipy, the reference's own algorithm)
-          on the host cores, one frame.
+          on the host cores, one frame, workers = cpu_count and workers = 1.
 cufft     the same loop written with torch.fft.rfft2/irfft2 (cuFFT) and
           torch elementwise ops in fp32, one CUDA graph per step,
           timed in the same run; its output is checked against ours.
@@ -47,9 +57,29 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
+
 H, W, CH, ITERS = 1080, 1920, 3, 4
 P_EXP, EPS, LAM = 0.8, 1e-4, 1.0
 METRIC = "1080p colour ILS frames/s (4 iters) on 1/2/4/8 B200; HBM roofline fraction"
+WORKLOAD = "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters"
+
+
+def config_of(world):
+    """The `config` both arms print (identical dicts)."""
+    return {"workload": WORKLOAD, "parallelism": f"frame-sharded x{world}",
+            "l2": "inputs larger than L2 (16 frames x 24.9 MB per step per GPU)"}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def bytes_per_frame(iters=ITERS, h=H, w=W, ch=CH):
@@ -163,11 +193,11 @@ def cufft_loop(f, lam, iters, p, eps, c):
     return u
 
 
-def cpu_port_frame_seconds(frames=1, seed=20240607, warm=True):
+def cpu_port_frame_seconds(frames=1, seed=20240607, warm=True, workers=None):
     """Oracle port (the reference algorithm, numpy + scipy.fft) on one 1080p RGB frame."""
     from oracle import ils_oracle as O
 
-    workers = os.cpu_count() or 1
+    workers = workers or os.cpu_count() or 1
     planes = O.bench_planes(H, W, CH, seed=seed)
     pen = O.Charbonnier(P_EXP, EPS)
     if warm:
@@ -178,30 +208,193 @@ def cpu_port_frame_seconds(frames=1, seed=20240607, warm=True):
     return (time.perf_counter() - t0) / frames, workers
 
 
+SAMPLE = ("1 frame (3 planes 1920x1080) per step, oracle port of smooth_color: channels on a 3-thread pool, "
+          "scipy.fft workers=cpu_count (smoother.py:208-210)")
+
+
 def run_reference(args, rank):
     """--impl reference: the reference's algorithm on host cores (oracle port)."""
     if rank != 0:
         return
-    sec, workers = cpu_port_frame_seconds(frames=1)  # warm-up + one sample
+    warm = max(1, min(args.warmup, 5))
+    for _ in range(warm):
+        cpu_port_frame_seconds(frames=1, warm=False)
     samples = []
-    # each step is one 1080p RGB frame (~1 s on 16 cores): cap the sample so
+    # each step is one 1080p RGB frame (~0.4 s on 16 cores): cap the sample so
     # the reference arm finishes within a few minutes at any --steps
     for _ in range(max(1, min(args.steps, 30))):
-        s, _ = cpu_port_frame_seconds(frames=1, warm=False)
+        s, workers = cpu_port_frame_seconds(frames=1, warm=False)
         samples.append(s)
     mean = sum(samples) / len(samples)
     fps = 1.0 / mean
+    s1, _ = cpu_port_frame_seconds(frames=1, warm=False, workers=1)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(fps, 4), "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": len(samples), "warmup": 1, "ms_per_step": round(mean * 1e3, 3),
+        "n_gpus": args.gpus, "steps": len(samples), "warmup": warm, "ms_per_step": round(mean * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
-                   "frames_per_step": 1, "impl": "oracle port of ilsmooth.smooth_color (numpy/scipy.fft)"},
+        "config": config_of(world),
         "cpu_baseline": {"value": round(fps, 4), "unit": "frames/s", "cores": workers, "kind": "port",
-                         "sample": "1 frame (3 planes 1920x1080) per step; channels on a 3-thread pool, scipy.fft workers=cpu_count (smoother.py:208-210)"},
+                         "sample": SAMPLE, "cpu_model": cpu_model(),
+                         "workers_1": {"value": round(1.0 / s1, 4), "unit": "frames/s", "cores": 1}},
         "e2e": {"value": round(fps, 4), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl_detail": "oracle port of ilsmooth.smooth_color (numpy/scipy.fft); the reference is pure Python "
+                       "and cannot travel to the GPU box",
     }
     print(json.dumps(line), flush=True)
+
+
+def c4_leg(args, world, rank, dev, barrier, max_over_ranks):
+    """C4: 3840x2160 RGB frames, Charbonnier N=4, args.c4_frames frames split over the ranks
+    (no communication); aggregate frames/s over one pass of the whole batch, max over ranks.
+
+    Frame k's input is generated from seed 20240607 + k on the rank that owns it; 16 distinct
+    input frames (1.6 GB, far above L2) are cycled through so the batch fits any HBM budget.
+    """
+    import torch
+
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+    from paper_2003_07504_b200 import dist as D
+    from paper_2003_07504_b200.penalty import params_of
+
+    h, w, ch = 2160, 3840, 3
+    mine = D.frame_shard(args.c4_frames, world, rank)
+    prm = ils.SmoothParams(ils.Charbonnier(P_EXP, EPS), LAM, iters=ITERS)
+    plan = rt.get_plan(ch, h, w, params_of(prm), _lib.ILS_F32, dev.index)
+    L = _lib.lib()
+    nin = min(16, len(mine))
+    frames = torch.empty((nin, ch, h, w), device=dev)
+    for i in range(nin):
+        g = torch.Generator(device=dev)
+        g.manual_seed(20240607 + mine[i])
+        frames[i] = torch.rand((ch, h, w), generator=g, device=dev)
+    out = torch.empty_like(frames)
+    lanes = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev) for _ in lanes]
+    sts = [torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev) for _ in lanes]
+
+    def run_all():
+        cur = torch.cuda.current_stream(dev)
+        for ln in lanes:
+            ln.wait_stream(cur)
+        for i in range(len(mine)):
+            k = i % 2
+            j = i % nin
+            _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(frames[j].data_ptr()), C.c_void_p(out[j].data_ptr()), h * w,
+                                    C.c_void_p(wss[k].data_ptr()), C.c_void_p(lanes[k].cuda_stream),
+                                    C.c_void_p(sts[k].data_ptr()), None), "ils_smooth")
+        for ln in lanes:
+            cur.wait_stream(ln)
+
+    run_all()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 2
+    e0.record()
+    for _ in range(reps):
+        run_all()
+    e1.record()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+    for st in sts:
+        rt.raise_status(int(st.item()))
+    # placement invariance: frame 0 of this rank smoothed alone equals its batch result
+    alone = ils.smooth_batch(frames[0], prm)
+    same = bool(torch.equal(alone, out[0]))
+    fps = args.c4_frames / (ms / 1e3)
+    peak, _ = peaks()
+    bpf = bytes_per_frame(ITERS, h, w, ch)
+    del frames, out
+    torch.cuda.empty_cache()
+    return {"workload": "C4: 3840x2160 RGB video, 256 frames, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
+            "value": round(fps, 2), "unit": "frames/s", "frames": args.c4_frames, "n_gpus": world,
+            "scaling": "strong (fixed 256-frame batch split over the ranks, no communication)",
+            "ms_per_batch": round(ms, 3), "whole_path": {"achieved": round(bpf * fps / world / 1e9, 1),
+                                                         "frac": round(bpf * fps / world / 1e9 / peak, 4),
+                                                         "bytes_per_frame": bpf},
+            "bitwise_equal_alone_vs_batched": same}
+
+
+def c5_leg(args, world, rank, local, dev, barrier, max_over_ranks):
+    """C5: one 7680x4320 RGB image, Welsch gamma=10/255, lambda=30, N=10, c=2: ms per image.
+
+    One rank: ils_smooth on the three planes.  N > 1 ranks: the row-slab
+    decomposition with the transposes as NCCL all-to-alls (dist.SlabPipeline,
+    the exchanges of one plane overlapping the other planes' passes); the
+    result is checked bitwise against the 1-GPU smooth on every rank's rows.
+    """
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+    from paper_2003_07504_b200 import dist as D
+    from paper_2003_07504_b200.penalty import params_of
+
+    h, w = 4320, 7680
+    prm = ils.SmoothParams(ils.Welsch(10 / 255), 30.0, iters=10, c=2.0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(20240607)
+    img = torch.rand((3, h, w), generator=g, device=dev)  # the same image on every rank
+    L = _lib.lib()
+    steps = 5
+    if world == 1:
+        plan = rt.get_plan(3, h, w, params_of(prm), _lib.ILS_F32, local)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        st = torch.empty(1, dtype=torch.int32, device=dev)
+        u = torch.empty_like(img)
+
+        def step():
+            _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(img.data_ptr()), C.c_void_p(u.data_ptr()), h * w,
+                                    C.c_void_p(ws.data_ptr()), C.c_void_p(torch.cuda.current_stream(dev).cuda_stream),
+                                    C.c_void_p(st.data_ptr()), None), "ils_smooth")
+        mode = "single GPU (ils_smooth, 3 planes batched)"
+    else:
+        splan, lay = D.slab_layout(h, w, params_of(prm), _lib.ILS_F32, world, rank, device=local)
+        stream = lambda: torch.cuda.current_stream(dev).cuda_stream  # noqa: E731
+        alloc = lambda n: torch.zeros(n, dtype=torch.float32, device=dev)  # noqa: E731
+        pipe = D.SlabPipeline(lay, prm.iters, D.CudaSlabKernels(splan, stream), D.torch_exchange_async(), alloc,
+                              planes=3)
+        rows = D.halo_rows(h, lay.row0[rank], lay.row0[rank + 1])
+        f_ext = [img[c][rows].contiguous() for c in range(3)]
+        us = [torch.empty((lay.rows, w), device=dev) for _ in range(3)]
+        st = torch.empty(1, dtype=torch.int32, device=dev)
+
+        def step():
+            st.fill_(_lib.STATUS_CLEAN)
+            pipe.smooth(f_ext, us, st)
+        mode = f"row slabs over {world} ranks, NCCL all-to-all transposes (SlabPipeline)"
+    for _ in range(2):
+        step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    rt.raise_status(int(st.item()))
+    ref = ils.smooth_batch(img, prm)  # the 1-GPU result
+    if world == 1:
+        same = bool(torch.equal(ref, u))
+    else:
+        r0, r1 = lay.row0[rank], lay.row0[rank + 1]
+        ok = torch.tensor([1 if all(torch.equal(us[c], ref[c, r0:r1]) for c in range(3)) else 0], device=dev)
+        tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)
+        same = bool(ok.item())
+        _lib.lib().ils_plan_destroy(splan)
+    peak, _ = peaks()
+    bpi = bytes_per_frame(10, h, w, 3)
+    del img, ref
+    torch.cuda.empty_cache()
+    return {"workload": "C5: 7680x4320 RGB image, Welsch gamma=10/255 lambda=30 c=2, 10 iters",
+            "value": round(ms, 3), "unit": "ms per image", "higher_is_better": False, "n_gpus": world,
+            "mode": mode, "images_per_s": round(1e3 / ms, 2),
+            "whole_path": {"achieved": round(bpi / (ms / 1e3) / world / 1e9, 1),
+                           "frac": round(bpi / (ms / 1e3) / world / 1e9 / peak, 4), "bytes_per_image": bpi},
+            "bitwise_equal_to_1gpu": same}
 
 
 def main():
@@ -216,6 +409,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT + torch comparison leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (4K video) leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (8K image) leg")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the numpy drop-in (smooth_color) leg")
+    ap.add_argument("--c4-frames", type=int, default=256)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -230,6 +427,7 @@ def main():
 
     import paper_2003_07504_b200 as ils
     from paper_2003_07504_b200 import _lib, _runtime as rt
+    from paper_2003_07504_b200.penalty import params_of
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -252,7 +450,7 @@ def main():
     G = max(1, min(args.group, F))
     assert F % G == 0, "--frames must be a multiple of --group"
     params = ils.SmoothParams(ils.Charbonnier(P_EXP, EPS), LAM, iters=ITERS)
-    cp = params.c_params()
+    cp = params_of(params)
     gen = torch.Generator(device=dev)
     gen.manual_seed(20240607 + rank)
     f = torch.rand((F * CH, H, W), generator=gen, device=dev, dtype=torch.float32)
@@ -412,13 +610,14 @@ def main():
         b.record(stream)
         barrier()
         ms_e2e = max_over_ranks(a.elapsed_time(b) / e2e_steps)
-        if u8:  # the fused 8-bit path equals the device path on the same frames
-            got = ils.smooth_frames_u8(fd8[:G], params)
-            assert torch.equal(uh[:G].to(dev), got), "e2e output differs from device path"
+        # every frame of the host pipeline (both lanes, all I/O slots) equals the device path
+        if u8:
+            got = ils.smooth_frames_u8(fd8, params)
+            assert torch.equal(uh.to(dev), got), "e2e output differs from device path"
             nbytes = F * CH * H * W
             api = "ils_smooth_host_u8 (C ABI): pinned host 8-bit RGB frames in and out (the reference's PNG/PPM pixel path)"
         else:
-            assert torch.equal(uh[:CH].to(dev), u[:CH]), "e2e output differs from device path"
+            assert torch.equal(uh.to(dev), u), "e2e output differs from device path"
             nbytes = F * CH * H * W * 4
             api = "ils_smooth_host (C ABI): pinned host fp32 planes in and out"
         return {"value": round(world * F / (ms_e2e / 1e3), 2), "unit": "frames/s",
@@ -457,11 +656,63 @@ def main():
                  "max_abs_diff_vs_ours": diff}
         del ref_u
 
+    # ---- parity of this run's frame 0 against the float64 oracle (north star: 1e-4, 60 dB)
+    parity = None
+    if rank == 0:
+        from oracle import ils_oracle as O
+
+        f0 = f[:CH].double().cpu().numpy()
+        u0 = u[:CH].double().cpu().numpy()
+        worst, psnr = 0.0, float("inf")
+        for c in range(CH):
+            ref = O.smooth_plane(f0[c], O.Charbonnier(P_EXP, EPS), LAM, ITERS, workers=os.cpu_count() or 1)
+            worst = max(worst, float(np.max(np.abs(u0[c] - ref))))
+            psnr = min(psnr, O.psnr(u0[c], ref))
+        parity = {"frame": 0, "max_abs": worst, "psnr_db": round(psnr, 2), "vs": "float64 oracle (numpy/scipy)",
+                  "tolerance": {"max_abs": 1e-4, "psnr_db": 60.0}, "ok": bool(worst <= 1e-4 and psnr >= 60.0)}
+
+    # ---- the reference's entry point: smooth_color on float64 numpy planes
+    dropin = None
+    if not args.no_dropin:
+        rng = np.random.default_rng(20240607 + rank)
+        imgs = [ils.MultiImage(tuple(rng.random((H, W)) for _ in range(CH)), ils.RGB) for _ in range(2)]
+        for i in range(max(2, args.warmup)):
+            ils.smooth_color(imgs[i % 2], params)
+        n_calls = max(4, min(args.steps, 40))
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record()
+        for i in range(n_calls):
+            out_img = ils.smooth_color(imgs[i % 2], params)
+        b.record()
+        barrier()
+        wall = (time.perf_counter() - t0) / n_calls
+        ms_call = max_over_ranks(max(a.elapsed_time(b) / n_calls, wall * 1e3))
+        nb = CH * H * W * 8
+        dropin = {"value": round(world / (ms_call / 1e3), 2), "unit": "frames/s", "ms_per_call": round(ms_call, 3),
+                  "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb + 4,
+                  "api": "paper_2003_07504_b200.smooth_color(MultiImage of 3 float64 numpy planes) -> MultiImage "
+                         "(the reference's entry point, smoother.py:175-217), one image per call",
+                  "output_dtype": str(out_img.channels[0].dtype)}
+
+    # ---- C4: 3840x2160 RGB video, 256 frames sharded over the ranks (BASELINE.json configs[3])
+    c4 = None
+    if not args.no_c4:
+        c4 = c4_leg(args, world, rank, dev, barrier, max_over_ranks)
+
+    # ---- C5: one 7680x4320 RGB image, Welsch N=10 (BASELINE.json configs[4])
+    c5 = None
+    if not args.no_c5:
+        c5 = c5_leg(args, world, rank, local, dev, barrier, max_over_ranks)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sec, workers = cpu_port_frame_seconds(frames=1)
+        sec1, _ = cpu_port_frame_seconds(frames=1, warm=False, workers=1)
         cpu = {"value": round(1.0 / sec, 4), "unit": "frames/s", "cores": workers, "kind": "port",
-               "sample": "1 frame (3 planes 1920x1080), oracle port of smooth_color: channels on a 3-thread pool, scipy.fft workers=cpu_count (smoother.py:208-210)"}
+               "sample": SAMPLE, "cpu_model": cpu_model(),
+               "workers_1": {"value": round(1.0 / sec1, 4), "unit": "frames/s", "cores": 1}}
 
     if rank == 0:
         bpf = bytes_per_frame()
@@ -472,13 +723,16 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
-                       "frames_per_step_per_gpu": F, "frames_per_launch_group": G, "streams": S,
-                       "parallelism": f"frame-sharded x{world}", "l2": "inputs larger than L2 (F x 24.9 MB)",
-                       "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec", "col2_spec",
-                                                          "col2_n1", "col2_n2", "col2_cols")}},
+            "config": config_of(world),
+            "step": {"frames_per_step_per_gpu": F, "frames_per_launch_group": G, "streams": S},
+            "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec", "col2_spec",
+                                               "col2_n1", "col2_n2", "col2_cols")},
             "e2e": e2e,
             "e2e_f32_planes": e2e_f32,
+            "e2e_dropin": dropin,
+            "parity": parity,
+            "c4": c4,
+            "c5": c5,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": round(row_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(row_gbs / peak, 4), "traffic": measured_traffic("k_row_it"),

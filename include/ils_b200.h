@@ -177,6 +177,32 @@ ILS_API ils_status ils_irfft2(const ils_plan* plan, void* spec_dev, int64_t spec
 ILS_API ils_status ils_rgb_yuv(void* planes_dev, int32_t dtype, int64_t plane_stride, int64_t npx, int32_t frames,
                        int32_t inverse, void* stream);
 
+/* ---- standalone field kernels (the reference exports these steps as
+ * functions, __init__.py:44-61; inside ils_smooth they are fused into the row
+ * pass and never touch memory).  Planar [batch][height][width], plane_stride
+ * elements apart, dtype ILS_F32/ILS_F64, asynchronous on `stream`.  The fp64
+ * gradients and adjoint are bit-identical to the reference's numpy. */
+/* grad_x / grad_y (solver.py:33-40): periodic forward differences; gx or gy may be NULL. */
+ILS_API ils_status ils_grad(const void* u_dev, void* gx_dev, void* gy_dev, int32_t batch, int32_t height,
+                            int32_t width, int64_t plane_stride, int32_t dtype, void* stream);
+/* adjoint_accumulate (solver.py:43-49): roll(mu_x,1,1) - mu_x + roll(mu_y,1,0) - mu_y. */
+ILS_API ils_status ils_adjoint_accumulate(const void* mu_x_dev, const void* mu_y_dev, void* out_dev, int32_t batch,
+                                          int32_t height, int32_t width, int64_t plane_stride, int32_t dtype,
+                                          void* stream);
+/* aux_update (penalty.py:117-126): out = c x - phi'(x) over n elements; params
+ * kind/p/eps/gamma/c (c checked against the penalty's minimum curvature,
+ * penalty.py:108-114, -> ILS_EINVAL); lam and iters must be valid but unused. */
+ILS_API ils_status ils_aux_update(const ils_params* params, const void* x_dev, void* out_dev, int64_t n,
+                                  int32_t dtype, void* stream);
+/* energy (smoother.py:93-101): out_dev[b] = sum (u-f)^2 + lam (sum phi(grad_x u) +
+ * sum phi(grad_y u)) per plane, f64, deterministic.  Only the penalty fields of
+ * params are validated (lam: any finite value; c, iters unused).  scratch:
+ * ILS_ENERGY_SCRATCH(batch) bytes of device memory. */
+#define ILS_ENERGY_SCRATCH(batch) ((size_t)(batch) * 256u * 3u * sizeof(double))
+ILS_API ils_status ils_energy(const ils_params* params, const void* u_dev, const void* f_dev, int32_t batch,
+                              int32_t height, int32_t width, int64_t plane_stride, int32_t dtype, double* out_dev,
+                              void* scratch, void* stream);
+
 /* ---- C5: one image slab-decomposed over nranks GPUs --------
  * Rank r owns rows [row0[r], row0[r+1]) for the row passes and spectrum
  * columns [col0[r], col0[r+1]) for the column passes.  Between them the

@@ -13,9 +13,9 @@ from .image import GRAY, RGB, YUV, ColorMode, MultiImage, as_plane, clip01, lumi
 from .applications import (DetailBoost, TonemapParams, clipart_clean, detail_enhance, gaussian_blur,
                            texture_smooth, tonemap_multi, tonemap_single)
 from .hqs import HqsParams, hqs_smooth_batch, hqs_smooth_plane
-from .penalty import DEFAULT_EPS, Charbonnier, Welsch, check_curvature, huber, soft_threshold
-from .smoother import EnergyTrace, SmoothParams, smooth_batch, smooth_color, smooth_frames_u8, smooth_plane
-from .solver import SolverPlan, make_plan, solve_ls
+from .penalty import DEFAULT_EPS, Charbonnier, Welsch, aux_update, check_curvature, huber, soft_threshold
+from .smoother import EnergyTrace, SmoothParams, energy, smooth_batch, smooth_color, smooth_frames_u8, smooth_plane
+from .solver import SolverPlan, adjoint_accumulate, grad_x, grad_y, make_plan, solve_ls
 
 __version__ = "0.1.0"
 
@@ -26,4 +26,5 @@ __all__ = [
     "MultiImage", "NumericalError", "SmoothParams", "SolverPlan", "Welsch", "as_plane", "check_curvature",
     "get_default_precision", "hqs_smooth_batch", "hqs_smooth_plane", "huber", "make_plan", "rgb_to_yuv", "set_default_precision", "smooth_batch", "smooth_color", "smooth_frames_u8",
     "smooth_plane", "soft_threshold", "solve_ls", "yuv_to_rgb",
+    "adjoint_accumulate", "aux_update", "energy", "grad_x", "grad_y",
 ]

@@ -28,7 +28,7 @@ EXPORTS = (
     "ils_host_io_size", "ils_launch_pass", "ils_slab_plan_create", "ils_slab_get_layout", "ils_slab_row_pass",
     "ils_slab_col_pass",
     "ils_solve_ls", "ils_rfft2", "ils_irfft2", "ils_rgb_yuv", "ils_plan_get_info", "ils_last_error",
-    "ils_abi_version",
+    "ils_abi_version", "ils_grad", "ils_adjoint_accumulate", "ils_aux_update", "ils_energy",
 )
 
 
@@ -96,6 +96,11 @@ _SIGS = {
                                       C.POINTER(C.c_int64)]),
     "ils_slab_row_pass": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P]),
     "ils_slab_col_pass": (C.c_int, [_P, _P, _P, _P]),
+    "ils_grad": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _P]),
+    "ils_adjoint_accumulate": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _P]),
+    "ils_aux_update": (C.c_int, [C.POINTER(Params), _P, _P, C.c_int64, C.c_int32, _P]),
+    "ils_energy": (C.c_int, [C.POINTER(Params), _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _P,
+                             _P, _P]),
     "ils_last_error": (C.c_char_p, []),
     "ils_abi_version": (C.c_int32, []),
 }

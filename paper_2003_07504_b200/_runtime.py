@@ -101,6 +101,17 @@ def get_plan(batch, height, width, cparams, dtype_code, device_index) -> DeviceP
         return plan
 
 
+def plan_supported(height, width, precision) -> bool:
+    """Whether the planner has a launch configuration for this plane size (host-only plan, no GPU work)."""
+    L = _lib.lib()
+    h = C.c_void_p()
+    code = _lib.ILS_F32 if precision == "fp32" else _lib.ILS_F64
+    st = L.ils_plan_create(C.byref(h), 1, height, width, C.byref(_dummy_params()), code, -1)
+    if st == _lib.ILS_OK:
+        L.ils_plan_destroy(h)
+    return st == _lib.ILS_OK
+
+
 def _stream_ptr(torch, device):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -121,19 +132,31 @@ def smooth_device(f, cparams, trace=False, check=True):
     code = _lib.ILS_F32 if f.dtype == torch.float32 else _lib.ILS_F64
     if f.dtype not in (torch.float32, torch.float64):
         raise ValueError(f"unsupported dtype {f.dtype}")
+    f = _aligned(f)
     dev = f.device
-    plan = get_plan(B, H, W, cparams, code, dev.index if dev.index is not None else torch.cuda.current_device())
-    u = torch.empty_like(f)
-    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
-    status = torch.empty(1, dtype=torch.int32, device=dev)
-    energies = torch.empty((cparams.iters + 1, B), dtype=torch.float64, device=dev) if trace else None
-    L = _lib.lib()
-    _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()), H * W,
-                            C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev), C.c_void_p(status.data_ptr()),
-                            C.c_void_p(energies.data_ptr()) if trace else None), "ils_smooth")
+    plan = get_plan(B, H, W, cparams, code, _dev_index(torch, dev))
+    with torch.cuda.device(dev):
+        u = torch.empty_like(f)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+        energies = torch.empty((cparams.iters + 1, B), dtype=torch.float64, device=dev) if trace else None
+        L = _lib.lib()
+        _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()), H * W,
+                                C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev), C.c_void_p(status.data_ptr()),
+                                C.c_void_p(energies.data_ptr()) if trace else None), "ils_smooth")
     if check:
         raise_status(int(status.item()))
     return u, energies, status
+
+
+def _dev_index(torch, dev):
+    return dev.index if dev.index is not None else torch.cuda.current_device()
+
+
+def _aligned(t):
+    """The row passes move whole rows with TMA bulk copies (16-byte aligned
+    rows): a view at an odd storage offset is copied into fresh storage."""
+    return t if t.data_ptr() % 16 == 0 else t.clone()
 
 
 def raise_status(s: int) -> None:
@@ -147,19 +170,24 @@ def raise_status(s: int) -> None:
 def solve_device(f, mx, my, cparams):
     """solve_ls on CUDA tensors [B, H, W] (solver.py:109-134)."""
     torch = _torch()
-    f, mx, my = (t.contiguous() for t in (f, mx, my))
+    f, mx, my = (_aligned(t.contiguous()) for t in (f, mx, my))
+    if not (f.shape == mx.shape == my.shape and f.dtype == mx.dtype == my.dtype and f.device == mx.device == my.device):
+        raise ValueError("f, mu_x and mu_y must share shape, dtype and device")
+    if f.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"unsupported dtype {f.dtype}")
     B, H, W = f.shape
     code = _lib.ILS_F32 if f.dtype == torch.float32 else _lib.ILS_F64
     dev = f.device
-    plan = get_plan(B, H, W, cparams, code, dev.index if dev.index is not None else torch.cuda.current_device())
-    u = torch.empty_like(f)
-    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
-    status = torch.empty(1, dtype=torch.int32, device=dev)
-    L = _lib.lib()
-    _lib.check(L.ils_solve_ls(plan.ptr, C.c_void_p(f.data_ptr()), C.c_void_p(mx.data_ptr()),
-                              C.c_void_p(my.data_ptr()), C.c_void_p(u.data_ptr()), H * W,
-                              C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev), C.c_void_p(status.data_ptr())),
-               "ils_solve_ls")
+    plan = get_plan(B, H, W, cparams, code, _dev_index(torch, dev))
+    with torch.cuda.device(dev):
+        u = torch.empty_like(f)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+        L = _lib.lib()
+        _lib.check(L.ils_solve_ls(plan.ptr, C.c_void_p(f.data_ptr()), C.c_void_p(mx.data_ptr()),
+                                  C.c_void_p(my.data_ptr()), C.c_void_p(u.data_ptr()), H * W,
+                                  C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev), C.c_void_p(status.data_ptr())),
+                   "ils_solve_ls")
     s = int(status.item())
     if s != _lib.STATUS_CLEAN:
         raise NumericalError(f"non-finite values in {('f', 'mu_x', 'mu_y')[s - 1]}")
@@ -169,16 +197,17 @@ def solve_device(f, mx, my, cparams):
 def rfft2_device(x, cparams=None):
     """Hand-written real 2-D FFT of x[B, H, W] -> complex [B, H, W//2+1]."""
     torch = _torch()
-    x = x.contiguous()
+    x = _aligned(x.contiguous())
     B, H, W = x.shape
     code = _lib.ILS_F32 if x.dtype == torch.float32 else _lib.ILS_F64
     cparams = cparams or _dummy_params()
-    plan = get_plan(B, H, W, cparams, code, x.device.index or 0)
+    plan = get_plan(B, H, W, cparams, code, _dev_index(torch, x.device))
     pitch = plan.info["spec_pitch"]
     cdt = torch.complex64 if code == _lib.ILS_F32 else torch.complex128
-    spec = torch.empty((B, H, pitch), dtype=cdt, device=x.device)
-    _lib.check(_lib.lib().ils_rfft2(plan.ptr, C.c_void_p(x.data_ptr()), H * W, C.c_void_p(spec.data_ptr()), pitch,
-                                    _stream_ptr(torch, x.device)), "ils_rfft2")
+    with torch.cuda.device(x.device):
+        spec = torch.empty((B, H, pitch), dtype=cdt, device=x.device)
+        _lib.check(_lib.lib().ils_rfft2(plan.ptr, C.c_void_p(x.data_ptr()), H * W, C.c_void_p(spec.data_ptr()),
+                                        pitch, _stream_ptr(torch, x.device)), "ils_rfft2")
     return spec[:, :, : W // 2 + 1]
 
 
@@ -188,14 +217,15 @@ def irfft2_device(spec, width, cparams=None):
     B, H, Wc = spec.shape
     code = _lib.ILS_F32 if spec.dtype == torch.complex64 else _lib.ILS_F64
     cparams = cparams or _dummy_params()
-    plan = get_plan(B, H, width, cparams, code, spec.device.index or 0)
+    plan = get_plan(B, H, width, cparams, code, _dev_index(torch, spec.device))
     pitch = plan.info["spec_pitch"]
-    buf = torch.zeros((B, H, pitch), dtype=spec.dtype, device=spec.device)
-    buf[:, :, :Wc] = spec
-    rdt = torch.float32 if code == _lib.ILS_F32 else torch.float64
-    x = torch.empty((B, H, width), dtype=rdt, device=spec.device)
-    _lib.check(_lib.lib().ils_irfft2(plan.ptr, C.c_void_p(buf.data_ptr()), pitch, C.c_void_p(x.data_ptr()),
-                                     H * width, _stream_ptr(torch, spec.device)), "ils_irfft2")
+    with torch.cuda.device(spec.device):
+        buf = torch.zeros((B, H, pitch), dtype=spec.dtype, device=spec.device)
+        buf[:, :, :Wc] = spec
+        rdt = torch.float32 if code == _lib.ILS_F32 else torch.float64
+        x = torch.empty((B, H, width), dtype=rdt, device=spec.device)
+        _lib.check(_lib.lib().ils_irfft2(plan.ptr, C.c_void_p(buf.data_ptr()), pitch, C.c_void_p(x.data_ptr()),
+                                         H * width, _stream_ptr(torch, spec.device)), "ils_irfft2")
     return x
 
 
@@ -230,16 +260,33 @@ def _host_pool():
 
 
 def _pinned(name, shape, dtype):
+    """Per-thread pinned staging buffer `name`, reused across calls.
+
+    A buffer handed out again first waits for the asynchronous copy that last
+    read or wrote it (the event recorded by _pinned_done), so a host write
+    into it can never race an in-flight DMA of the previous call.
+    """
     torch = _torch()
     cache = getattr(_tls, "pinned", None)
     if cache is None:
         cache = _tls.pinned = {}
-    buf = cache.get(name)
+    buf, ev = cache.get(name, (None, None))
+    if ev is not None:
+        ev.synchronize()
     n = int(np.prod(shape))
     if buf is None or buf.numel() < n or buf.dtype != dtype:
         buf = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
-        cache[name] = buf
+    cache[name] = (buf, None)
     return buf[:n].view(*shape)
+
+
+def _pinned_done(name, stream):
+    """Record that `stream`'s queued copy is the last user of staging buffer `name`."""
+    torch = _torch()
+    buf, _ = _tls.pinned[name]
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    _tls.pinned[name] = (buf, ev)
 
 
 def _parallel(fn, n):
@@ -262,6 +309,7 @@ def to_device_planes(planes, precision=None):
     host = stage.numpy()
     _parallel(lambda i: np.copyto(host[i], arrs[i]), B)
     dev = stage.to("cuda", non_blocking=True)
+    _pinned_done("in", torch.cuda.current_stream())
     return dev if dt == torch.float64 else dev.to(dt)
 
 
@@ -272,7 +320,7 @@ def to_host_f64(t):
     B, H, W = t.shape
     stage = _pinned("out", (B, H, W), t.dtype)
     stage.copy_(t, non_blocking=True)
-    torch.cuda.current_stream(t.device).synchronize()
+    torch.cuda.current_stream(t.device).synchronize()  # the host reads the buffer next: nothing left in flight
     host = stage.numpy()
     out = [np.empty((H, W), dtype=np.float64) for _ in range(B)]
     _parallel(lambda i: np.copyto(out[i], host[i]), B)
@@ -293,13 +341,153 @@ def smooth_device_u8(frames, cparams, precision=None, check=True):
     F, H, W, Ch = frames.shape
     code = _lib.ILS_F32 if (precision or _PRECISION) == "fp32" else _lib.ILS_F64
     dev = frames.device
-    plan = get_plan(F * Ch, H, W, cparams, code, dev.index if dev.index is not None else torch.cuda.current_device())
-    u = torch.empty_like(frames)
-    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
-    status = torch.empty(1, dtype=torch.int32, device=dev)
-    _lib.check(_lib.lib().ils_smooth_u8(plan.ptr, C.c_void_p(frames.data_ptr()), C.c_void_p(u.data_ptr()), Ch,
-                                        C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev),
-                                        C.c_void_p(status.data_ptr())), "ils_smooth_u8")
+    plan = get_plan(F * Ch, H, W, cparams, code, _dev_index(torch, dev))
+    with torch.cuda.device(dev):
+        u = torch.empty_like(frames)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+        _lib.check(_lib.lib().ils_smooth_u8(plan.ptr, C.c_void_p(frames.data_ptr()), C.c_void_p(u.data_ptr()), Ch,
+                                            C.c_void_p(ws.data_ptr()), _stream_ptr(torch, dev),
+                                            C.c_void_p(status.data_ptr())), "ils_smooth_u8")
     if check:
         raise_status(int(status.item()))
     return u
+
+
+# Standalone field kernels (grad_x / grad_y / adjoint_accumulate / aux_update /
+# energy of the reference API): numpy in -> float64 on the device -> fresh
+# float64 numpy out; CUDA tensors in -> tensors of the same dtype out.
+def _as_field(a):
+    """(CUDA tensor [B, H, W] or [n], was_numpy, original shape)."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        if not a.is_cuda:
+            a = a.to("cuda")
+        if a.dtype not in (torch.float32, torch.float64):
+            a = a.to(torch.float64)
+        return a.contiguous(), False, tuple(a.shape)
+    arr = np.asarray(a, dtype=np.float64)
+    return torch.from_numpy(np.ascontiguousarray(arr)).to("cuda"), True, arr.shape
+
+
+def _planes3(t):
+    if t.dim() == 2:
+        return t.unsqueeze(0)
+    if t.dim() == 3:
+        return t
+    raise ValueError(f"expected a 2-D plane or a [B, H, W] stack, got shape {tuple(t.shape)}")
+
+
+def _dtype_code(t):
+    torch = _torch()
+    return _lib.ILS_F32 if t.dtype == torch.float32 else _lib.ILS_F64
+
+
+def _out(t, was_np, shape):
+    return t.cpu().numpy().reshape(shape) if was_np else t.reshape(shape)
+
+
+def grad_fields(u, which):
+    """which: 'x' or 'y' (solver.py:33-40)."""
+    torch = _torch()
+    t, was_np, shape = _as_field(u)
+    p = _planes3(t)
+    B, H, W = p.shape
+    out = torch.empty_like(p)
+    gx, gy = (out, None) if which == "x" else (None, out)
+    with torch.cuda.device(p.device):
+        _lib.check(_lib.lib().ils_grad(C.c_void_p(p.data_ptr()), C.c_void_p(gx.data_ptr()) if gx is not None else None,
+                                       C.c_void_p(gy.data_ptr()) if gy is not None else None, B, H, W, H * W,
+                                       _dtype_code(p), _stream_ptr(torch, p.device)), "ils_grad")
+    return _out(out, was_np, shape)
+
+
+def adjoint_fields(mu_x, mu_y):
+    """solver.py:43-49."""
+    torch = _torch()
+    tx, was_np, shape = _as_field(mu_x)
+    ty, _, shape_y = _as_field(mu_y)
+    if shape != shape_y:
+        raise ValueError(f"field shapes differ: {shape} vs {shape_y}")
+    if ty.dtype != tx.dtype:
+        ty = ty.to(tx.dtype)
+    px, py = _planes3(tx), _planes3(ty.to(tx.device))
+    B, H, W = px.shape
+    out = torch.empty_like(px)
+    with torch.cuda.device(px.device):
+        _lib.check(_lib.lib().ils_adjoint_accumulate(C.c_void_p(px.data_ptr()), C.c_void_p(py.data_ptr()),
+                                                     C.c_void_p(out.data_ptr()), B, H, W, H * W, _dtype_code(px),
+                                                     _stream_ptr(torch, px.device)), "ils_adjoint_accumulate")
+    return _out(out, was_np, shape)
+
+
+def aux_fields(cparams, x):
+    """penalty.py:117-126 on every element of x."""
+    torch = _torch()
+    t, was_np, shape = _as_field(x)
+    out = torch.empty_like(t)
+    with torch.cuda.device(t.device):
+        _lib.check(_lib.lib().ils_aux_update(C.byref(cparams), C.c_void_p(t.data_ptr()), C.c_void_p(out.data_ptr()),
+                                             t.numel(), _dtype_code(t), _stream_ptr(torch, t.device)),
+                   "ils_aux_update")
+    return _out(out, was_np, shape)
+
+
+def energy_fields(cparams, u, f):
+    """smoother.py:93-101: one float (2-D input) or a float64 tensor [B] (stacked tensors)."""
+    torch = _torch()
+    tu, was_np, shape = _as_field(u)
+    tf, _, shape_f = _as_field(f)
+    if shape != shape_f:
+        raise ValueError(f"shapes differ: u {shape}, f {shape_f}")
+    if tf.dtype != tu.dtype:
+        tf = tf.to(tu.dtype)
+    pu, pf = _planes3(tu), _planes3(tf.to(tu.device))
+    B, H, W = pu.shape
+    out = torch.empty(B, dtype=torch.float64, device=pu.device)
+    scratch = torch.empty(B * 256 * 3, dtype=torch.float64, device=pu.device)
+    with torch.cuda.device(pu.device):
+        _lib.check(_lib.lib().ils_energy(C.byref(cparams), C.c_void_p(pu.data_ptr()), C.c_void_p(pf.data_ptr()), B, H,
+                                         W, H * W, _dtype_code(pu), C.c_void_p(out.data_ptr()),
+                                         C.c_void_p(scratch.data_ptr()), _stream_ptr(torch, pu.device)), "ils_energy")
+    if len(shape) == 2:
+        return float(out[0].item())
+    return out
+
+
+def denominator(height, width, lam, c):
+    """SolverPlan.denom (solver.py:100-102) as a float64 numpy array, evaluated on the GPU."""
+    import math
+
+    torch = _torch()
+    with torch.no_grad():
+        kx = torch.arange(width, dtype=torch.float64, device="cuda")
+        ky = torch.arange(height, dtype=torch.float64, device="cuda")
+        wx = 2.0 - 2.0 * torch.cos(2.0 * math.pi * kx / width)
+        wy = 2.0 - 2.0 * torch.cos(2.0 * math.pi * ky / height)
+        d = 1.0 + (c * lam / 2.0) * (wy[:, None] + wx[None, :])
+    return d.cpu().numpy()
+
+
+def fft2_full(f):
+    """fft2 of a real plane as the reference caches it (SolverPlan.with_data,
+    solver.py:69-75): complex128 H x W, from the hand-written fp64 r2c on the
+    GPU, the other half filled in by Hermitian symmetry X[k1, k2] =
+    conj(X[-k1 mod H, W - k2])."""
+    torch = _torch()
+    x = torch.from_numpy(np.ascontiguousarray(np.asarray(f, dtype=np.float64))).to("cuda")
+    H, W = x.shape
+    try:
+        half = rfft2_device(x[None])[0]  # [H, W//2 + 1]
+    except ValueError:
+        # no fp64 plan for this size (fp64 lines stop at about 4096 points):
+        # the fp32 transform, widened (relative error ~1e-7)
+        half = rfft2_device(x[None].float())[0].to(torch.complex128)
+    Wc = W // 2 + 1
+    full = torch.empty((H, W), dtype=torch.complex128, device=x.device)
+    full[:, :Wc] = half
+    if W > Wc:
+        rows = (-torch.arange(H, device=x.device)) % H
+        cols = W - torch.arange(Wc, W, device=x.device)
+        full[:, Wc:] = half[rows][:, cols].conj()
+    return full.cpu().numpy()

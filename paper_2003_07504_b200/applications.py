@@ -27,7 +27,7 @@ import numpy as np
 from . import _lib, _runtime as rt
 from .errors import NumericalError
 from .image import GRAY, RGB, ColorMode, MultiImage, as_plane
-from .penalty import Welsch
+from .penalty import Welsch, is_luminance_only, params_of
 from .smoother import SmoothParams, smooth_color
 
 
@@ -83,7 +83,7 @@ def _smooth_epilogue(planes, params: SmoothParams, k: float):
     B, H, W = planes.shape
     code = _lib.ILS_F32 if planes.dtype == torch.float32 else _lib.ILS_F64
     dev = planes.device
-    plan = rt.get_plan(B, H, W, params.c_params(), code, dev.index if dev.index is not None else 0)
+    plan = rt.get_plan(B, H, W, params_of(params), code, dev.index if dev.index is not None else 0)
     out = torch.empty_like(planes)
     ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
     status = torch.empty(1, dtype=torch.int32, device=dev)
@@ -119,7 +119,7 @@ def detail_enhance(img: MultiImage, params: SmoothParams, boost: DetailBoost = D
     """applications.py:80-93: clip01(u + k (f - u)); k = 1 returns the input as-is."""
     if boost.k == 1.0:
         return img
-    if params.color_mode is ColorMode.LUMINANCE_ONLY and img.space == RGB:
+    if is_luminance_only(params) and img.space == RGB:
         # u comes from the YUV round trip (smooth_color on the GPU); the boost
         # is element-wise on the device in float64
         torch = rt._torch()
@@ -174,7 +174,7 @@ def _bases(log_lum64, params_list, precision):
     for i, (prm, st) in enumerate(zip(params_list, streams)):
         st.wait_stream(cur)
         with torch.cuda.stream(st):
-            u, _, status = rt.smooth_device(f, prm.c_params(), check=False)
+            u, _, status = rt.smooth_device(f, params_of(prm), check=False)
             outs[i] = u[0]
             statuses.append(status)
     for st in streams:

@@ -27,7 +27,7 @@ UNITS = ([("ils_api.cu", "api", [])]
          + [("ils_inst.cu", f"col_spec{i}", [f"-DILS_INST_COL_SPEC={i}"]) for i in range(N_COL_SPECS)]
          + [("ils_inst.cu", "col2", ["-DILS_INST_COL2", "-DILS_PACKED_F32X2"])])
 SOURCES = sorted({u[0] for u in UNITS})
-HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_col2.cuh", "ils_inst.cu"]
+HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_col2.cuh", "ils_elem.cuh", "ils_inst.cu"]
 BASE_HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh"]
 
 
@@ -36,6 +36,8 @@ def _unit_deps(src, tag):
     deps = [src] + BASE_HEADERS
     if tag in ("api", "col2"):
         deps.append("ils_col2.cuh")
+    if tag == "api":
+        deps.append("ils_elem.cuh")
     deps = [os.path.join(CSRC, d) for d in deps]
     deps.append(os.path.join(ROOT, "include", "ils_b200.h"))
     deps.append(os.path.abspath(__file__))

@@ -19,6 +19,7 @@
 #include "../../include/ils_b200.h"
 #include "ils_kernels.cuh"
 #include "ils_col2.cuh"
+#include "ils_elem.cuh"
 
 using namespace ils;
 
@@ -636,6 +637,7 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
     // writes the planar f on the way; otherwise a separate deinterleave kernel
     const bool fuse = std::is_same<T, float>::value && p->row_spec >= 0 && p->packed && p->W % 128 == 0 &&
                       ch == 3 && (size_t)p->LP * sizeof(cx<T>) >= (size_t)p->W * (ch + 1) &&
+                      reinterpret_cast<uintptr_t>(f8) % 16 == 0 &&
                       !env_int("ILS_NO_FUSED_INGEST", 0);
     if (fuse) {
       a.f8 = f8;
@@ -715,6 +717,39 @@ ils_status solve_t(const ils_plan* p, const T* f, const T* mx, const T* my, T* u
 
 ils_status plan_create_impl(ils_plan** out, int32_t batch, int32_t height, int32_t width, const ils_params* params,
                             int32_t dtype, int32_t device, double hqs_beta0, double hqs_kappa);
+
+// Runs an entry point on the plan's device (restoring the caller's current
+// device on exit), so a plan built for cuda:1 works whatever device the
+// calling thread has selected.
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) changed = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+// Plane buffers the row passes move as whole rows: packed plans load / store
+// sample pairs as one complex element (2 * sizeof(T) alignment, even plane
+// stride); compile-time fp32 plans move whole rows with TMA bulk copies
+// (16-byte aligned rows: pointer and plane stride in bytes multiples of 16).
+ils_status check_io(const ils_plan* p, const void* f, const void* u, int64_t ps) {
+  if (!p->packed) return ILS_OK;
+  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
+  const bool bulk = p->dtype == ILS_F32 && p->row_spec >= 0 && p->W % 8 == 0;
+  const size_t al = bulk ? 16 : 2 * es;
+  for (const void* q : {f, u})
+    if (q && reinterpret_cast<uintptr_t>(q) % al)
+      return fail(ILS_EINVAL, "plane buffer %p is not %zu-byte aligned (required for %dx%d planes)", q, al, p->H, p->W);
+  if (((size_t)ps * es) % al)
+    return fail(ILS_EINVAL, "plane_stride %lld elements is not a multiple of %zu bytes (required for %dx%d planes)",
+                (long long)ps, al, p->H, p->W);
+  return ILS_OK;
+}
+
 
 ils_status validate(const ils_params* q) {
   if (!q) return fail(ILS_EINVAL, "params is NULL");
@@ -943,6 +978,8 @@ ils_status ils_smooth(const ils_plan* p, const void* f, void* u, int64_t ps, voi
   if (p->slab) return fail(ILS_EINVAL, "slab plans run through ils_slab_row_pass / ils_slab_col_pass");
   if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
   if (energies && p->prm.kind == ILS_SOFT) return fail(ILS_EINVAL, "the penalty-splitting baseline has no energy trace");
+  if (ils_status st = check_io(p, f, u, ps)) return st;
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
     return smooth_t<float>(p, static_cast<const float*>(f), static_cast<float*>(u), ps, ws, s, status, energies);
@@ -958,6 +995,8 @@ ils_status ils_smooth_epilogue(const ils_plan* p, const void* f, void* u, int64_
   if (epi->kind != ILS_EPI_NONE && epi->kind != ILS_EPI_DETAIL) return fail(ILS_EINVAL, "unknown epilogue %d", epi->kind);
   if (!(epi->k >= 0.0 && std::isfinite(epi->k)))  // DetailBoost.__post_init__ (applications.py:29-31)
     return fail(ILS_EINVAL, "boost k must be finite and >= 0, got %g", epi->k);
+  if (ils_status st = check_io(p, f, u, ps)) return st;
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
     return smooth_t<float>(p, static_cast<const float*>(f), static_cast<float*>(u), ps, ws, s, status, nullptr,
@@ -1010,6 +1049,7 @@ ils_status ils_smooth_u8(const ils_plan* p, const uint8_t* f, uint8_t* u, int32_
   if (p->slab) return fail(ILS_EINVAL, "slab plans run through ils_slab_row_pass / ils_slab_col_pass");
   if (channels < 1 || p->B % channels != 0)
     return fail(ILS_EINVAL, "plan batch %d is not a whole number of %d-channel frames", p->B, channels);
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t ps = (int64_t)p->H * p->W;
   if (p->dtype == ILS_F32)
@@ -1022,6 +1062,9 @@ ils_status ils_solve_ls(const ils_plan* p, const void* f, const void* mx, const 
   if (!p || !f || !mx || !my || !u || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (ps < (int64_t)p->H * p->W) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
+  if (ils_status st = check_io(p, f, u, ps)) return st;
+  if (ils_status st = check_io(p, mx, my, ps)) return st;
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
     return solve_t<float>(p, static_cast<const float*>(f), static_cast<const float*>(mx),
@@ -1240,6 +1283,8 @@ ils_status ils_smooth_host(const ils_plan* p, const void* f_host, void* u_host, 
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
   if (ps != (int64_t)p->H * p->W) return fail(ILS_EINVAL, "host planes must be dense (plane_stride == H*W)");
+  if (ils_status st = check_io(p, ws, io_dev, ps)) return st;
+  DeviceGuard dg(p->device);
   const size_t bytes = (size_t)p->B * ps * (p->dtype == ILS_F32 ? 4 : 8);
   return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter, 0, 0,
                        [&](void* fd, void* ud, int32_t* st, void* w, cudaStream_t ls) {
@@ -1252,6 +1297,7 @@ ils_status ils_smooth_host_u8(const ils_plan* p, const uint8_t* f_host, uint8_t*
   if (!p || !f_host || !u_host || !ws || !io_dev) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (nbatches < 1) return fail(ILS_EINVAL, "nbatches must be >= 1");
+  DeviceGuard dg(p->device);
   const size_t bytes = (size_t)p->B * p->H * p->W;
   return host_pipeline(p, f_host, u_host, bytes, bytes, nbatches, ws, io_dev, stream, bad_iter, 1, channels,
                        [&](void* fd, void* ud, int32_t* st, void* w, cudaStream_t ls) {
@@ -1265,6 +1311,8 @@ ils_status ils_launch_pass(const ils_plan* p, int32_t pass, const void* f, void*
   if (!p || !ws || !status) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (pass < 0 || pass > 7 || pass == 4) return fail(ILS_EINVAL, "pass must be 0..3 or 5..7, got %d", pass);
+  if (ils_status st = check_io(p, f, u, ps)) return st;
+  DeviceGuard dg(p->device);
   const bool second = (pass & 4) != 0;
   pass &= 3;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1299,6 +1347,9 @@ ils_status ils_rfft2(const ils_plan* p, const void* x, int64_t ps, void* spec, i
   if (!p || !x || !spec) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (pitch < p->Wc) return fail(ILS_EINVAL, "spec_pitch %lld < width/2+1", (long long)pitch);
+  if (ils_status st = check_io(p, x, nullptr, ps)) return st;
+  if (pitch % 2 || reinterpret_cast<uintptr_t>(spec) % 16) return fail(ILS_EINVAL, "spectrum rows must be 16-byte aligned (even spec_pitch)");
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto run = [&](auto tag) -> ils_status {
     using T = decltype(tag);
@@ -1323,6 +1374,9 @@ ils_status ils_irfft2(const ils_plan* p, void* spec, int64_t pitch, void* x, int
   if (!p || !x || !spec) return fail(ILS_EINVAL, "NULL argument");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (pitch < p->Wc) return fail(ILS_EINVAL, "spec_pitch %lld < width/2+1", (long long)pitch);
+  if (ils_status st = check_io(p, nullptr, x, ps)) return st;
+  if (pitch % 2 || reinterpret_cast<uintptr_t>(spec) % 16) return fail(ILS_EINVAL, "spectrum rows must be 16-byte aligned (even spec_pitch)");
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto run = [&](auto tag) -> ils_status {
     using T = decltype(tag);
@@ -1355,6 +1409,114 @@ ils_status ils_rgb_yuv(void* planes, int32_t dtype, int64_t ps, int64_t npx, int
     k_rgb_yuv<float><<<blocks, 256, 0, s>>>(static_cast<float*>(planes), ps, npx, frames, inverse);
   else
     k_rgb_yuv<double><<<blocks, 256, 0, s>>>(static_cast<double*>(planes), ps, npx, frames, inverse);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+// ------------------------------------------------------------ standalone field kernels (drop-in API)
+}  // extern "C"
+
+namespace {
+template <typename T>
+PenaltyRef<T> pen_ref(const ils_params& q) {
+  PenaltyRef<T> P{};
+  P.kind = q.kind;
+  P.p = T(q.p);
+  P.eps = T(q.eps);
+  P.e = T(q.p / 2.0 - 1.0);
+  P.ph = T(q.p / 2.0);
+  P.g2x2 = T(2.0 * (q.gamma * q.gamma));
+  P.c = T(q.c);
+  P.lam = T(q.lam);
+  return P;
+}
+
+int elem_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8)); }
+
+ils_status check_planes(int32_t batch, int32_t height, int32_t width, int64_t ps, int32_t dtype) {
+  if (batch < 1 || height < 1 || width < 1) return fail(ILS_EINVAL, "invalid plane size %dx%d x %d", height, width, batch);
+  if (ps < (int64_t)height * width) return fail(ILS_EINVAL, "plane_stride %lld < H*W", (long long)ps);
+  if (dtype != ILS_F32 && dtype != ILS_F64) return fail(ILS_EINVAL, "unknown dtype %d", dtype);
+  return ILS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ils_status ils_grad(const void* u, void* gx, void* gy, int32_t batch, int32_t height, int32_t width, int64_t ps,
+                    int32_t dtype, void* stream) {
+  if (!u || (!gx && !gy)) return fail(ILS_EINVAL, "NULL argument");
+  ils_status st = check_planes(batch, height, width, ps, dtype);
+  if (st != ILS_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const dim3 grid(elem_blocks((long long)height * width), batch);
+  if (dtype == ILS_F32)
+    k_grad<float><<<grid, 256, 0, s>>>(static_cast<const float*>(u), static_cast<float*>(gx), static_cast<float*>(gy),
+                                       height, width, ps);
+  else
+    k_grad<double><<<grid, 256, 0, s>>>(static_cast<const double*>(u), static_cast<double*>(gx),
+                                        static_cast<double*>(gy), height, width, ps);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+ils_status ils_adjoint_accumulate(const void* mx, const void* my, void* out, int32_t batch, int32_t height,
+                                  int32_t width, int64_t ps, int32_t dtype, void* stream) {
+  if (!mx || !my || !out) return fail(ILS_EINVAL, "NULL argument");
+  ils_status st = check_planes(batch, height, width, ps, dtype);
+  if (st != ILS_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const dim3 grid(elem_blocks((long long)height * width), batch);
+  if (dtype == ILS_F32)
+    k_adjoint<float><<<grid, 256, 0, s>>>(static_cast<const float*>(mx), static_cast<const float*>(my),
+                                          static_cast<float*>(out), height, width, ps);
+  else
+    k_adjoint<double><<<grid, 256, 0, s>>>(static_cast<const double*>(mx), static_cast<const double*>(my),
+                                           static_cast<double*>(out), height, width, ps);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+ils_status ils_aux_update(const ils_params* q, const void* x, void* out, int64_t n, int32_t dtype, void* stream) {
+  if (!x || !out) return fail(ILS_EINVAL, "NULL argument");
+  ils_status st = validate(q);  // includes _check_curvature (penalty.py:108-114)
+  if (st != ILS_OK) return st;
+  if (n < 0 || (dtype != ILS_F32 && dtype != ILS_F64)) return fail(ILS_EINVAL, "bad aux_update arguments");
+  if (n == 0) return ILS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == ILS_F32)
+    k_aux<float><<<elem_blocks(n), 256, 0, s>>>(static_cast<const float*>(x), static_cast<float*>(out), n,
+                                                pen_ref<float>(*q));
+  else
+    k_aux<double><<<elem_blocks(n), 256, 0, s>>>(static_cast<const double*>(x), static_cast<double*>(out), n,
+                                                 pen_ref<double>(*q));
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+ils_status ils_energy(const ils_params* q, const void* u, const void* f, int32_t batch, int32_t height, int32_t width,
+                      int64_t ps, int32_t dtype, double* out, void* scratch, void* stream) {
+  if (!u || !f || !out || !scratch || !q) return fail(ILS_EINVAL, "NULL argument");
+  if (!std::isfinite(q->lam)) return fail(ILS_EINVAL, "lam must be finite, got %g", q->lam);
+  ils_params v = *q;  // energy needs the penalty only: lam / c / iters are not constrained here
+  v.lam = 1.0;
+  v.c = 1e300;
+  v.iters = 1;
+  ils_status st = validate(&v);
+  if (st != ILS_OK) return st;
+  st = check_planes(batch, height, width, ps, dtype);
+  if (st != ILS_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(scratch);
+  const dim3 grid(kEnergyBlocks, batch);
+  if (dtype == ILS_F32)
+    k_energy_part<float><<<grid, 256, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(f), height,
+                                              width, ps, pen_ref<float>(*q), part);
+  else
+    k_energy_part<double><<<grid, 256, 0, s>>>(static_cast<const double*>(u), static_cast<const double*>(f), height,
+                                               width, ps, pen_ref<double>(*q), part);
+  ILS_CUDA(cudaGetLastError());
+  k_energy_fin<<<batch, 256, 0, s>>>(part, kEnergyBlocks, q->lam, out);
   ILS_CUDA(cudaGetLastError());
   return ILS_OK;
 }
@@ -1553,6 +1715,7 @@ ils_status ils_slab_row_pass(const ils_plan* p, int32_t mode, const void* f_ext,
   if (mode != MODE_F0 && mode != MODE_IT && mode != MODE_FIN) return fail(ILS_EINVAL, "mode must be 0, 1 or 3");
   if (!status || (mode != MODE_FIN && !send) || (mode != MODE_F0 && !recv) || (mode == MODE_FIN && !u) || !f_ext)
     return fail(ILS_EINVAL, "NULL argument");
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
     return slab_row_t<float>(p, mode, static_cast<const float*>(f_ext), static_cast<const cx<float>*>(recv),
@@ -1565,6 +1728,7 @@ ils_status ils_slab_col_pass(const ils_plan* p, void* recv, void* send, void* st
   if (!p || !p->slab) return fail(ILS_EINVAL, "not a slab plan");
   if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
   if (!recv || !send) return fail(ILS_EINVAL, "NULL argument");
+  DeviceGuard dg(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->dtype == ILS_F32)
     return slab_col_t<float>(p, static_cast<cx<float>*>(recv), static_cast<cx<float>*>(send), s);

@@ -22,6 +22,7 @@ import ctypes as C
 from dataclasses import dataclass
 
 from . import _lib
+from .penalty import params_of
 
 _MAXSEG = 8
 
@@ -227,7 +228,7 @@ class EmulatedSlab:
         self.torch = torch
         self.P = nranks
         self.params = params
-        cp = params.c_params()
+        cp = params_of(params)
         self.plans, self.lays = [], []
         for r in range(nranks):
             h, lay = slab_layout(height, width, cp, dtype_code, nranks, r, device=device)

@@ -87,6 +87,17 @@ def check_curvature(spec, c: float) -> None:
         )
 
 
+def aux_update(spec, c: float, x):
+    """Optimal auxiliary variable c x - phi'(x), elementwise (penalty.py:117-126), on the GPU.
+
+    numpy in -> float64 numpy out; a CUDA tensor -> tensor of the same dtype.
+    """
+    check_curvature(spec, c)
+    from . import _runtime as rt
+
+    return rt.aux_fields(to_c_params(spec, 1.0, float(c), 1), x)
+
+
 def soft_threshold(x, alpha: float):
     """penalty.py:168-177 (host helper; the HQS field step runs fused in the row kernel)."""
     if not (alpha >= 0.0 and np.isfinite(alpha)):
@@ -103,12 +114,41 @@ def huber(x, alpha: float):
     return np.where(np.abs(x) <= alpha, x * x / (2.0 * alpha), np.abs(x) - alpha / 2.0)
 
 
+def penalty_kind(spec) -> str:
+    """'charbonnier' / 'welsch' for this package's penalties and for any object
+    with the reference's fields (the reference's own frozen dataclasses,
+    penalty.py:47-105), so reference parameter objects can be passed straight in."""
+    if isinstance(spec, Charbonnier):
+        return "charbonnier"
+    if isinstance(spec, Welsch):
+        return "welsch"
+    name = type(spec).__name__
+    if name == "Charbonnier" or (hasattr(spec, "p") and hasattr(spec, "eps") and not hasattr(spec, "gamma")):
+        return "charbonnier"
+    if name == "Welsch" or (hasattr(spec, "gamma") and not hasattr(spec, "p")):
+        return "welsch"
+    raise ValueError(f"unsupported penalty {name}: the CUDA path implements Charbonnier and Welsch")
+
+
 def to_c_params(spec, lam: float, c: float, iters: int):
     """Flatten (penalty, lam, c, iters) into the C ABI's ils_params."""
     from ._lib import ILS_CHARBONNIER, ILS_WELSCH, Params
 
-    if isinstance(spec, Charbonnier):
-        return Params(ILS_CHARBONNIER, spec.p, spec.eps, 0.0, float(lam), float(c), int(iters))
-    if isinstance(spec, Welsch):
-        return Params(ILS_WELSCH, 0.0, 0.0, spec.gamma, float(lam), float(c), int(iters))
-    raise ValueError(f"unsupported penalty {type(spec).__name__}: the CUDA path implements Charbonnier and Welsch")
+    if penalty_kind(spec) == "charbonnier":
+        return Params(ILS_CHARBONNIER, float(spec.p), float(spec.eps), 0.0, float(lam), float(c), int(iters))
+    return Params(ILS_WELSCH, 0.0, 0.0, float(spec.gamma), float(lam), float(c), int(iters))
+
+
+def params_of(params):
+    """ils_params of a SmoothParams -- this package's or the reference's
+    (smoother.py:31-62: .penalty, .lam, .iters, .c / .curvature)."""
+    c = getattr(params, "curvature", None)
+    if c is None:
+        c = params.penalty.min_curvature if params.c is None else float(params.c)
+    return to_c_params(params.penalty, params.lam, float(c), params.iters)
+
+
+def is_luminance_only(params) -> bool:
+    """ColorMode.LUMINANCE_ONLY of either package's enum (compared by value)."""
+    mode = getattr(params, "color_mode", None)
+    return getattr(mode, "value", mode) == "luminance_only"

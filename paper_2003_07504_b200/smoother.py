@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _runtime as rt
 from .image import GRAY, RGB, YUV, ColorMode, MultiImage, as_plane
-from .penalty import to_c_params
+from .penalty import is_luminance_only, params_of, to_c_params
 from .solver import SolverPlan, make_plan
 
 
@@ -74,6 +74,17 @@ class EnergyTrace:
         return (e0 - self.energies[n]) / den
 
 
+def energy(u, f, penalty, lam: float) -> float:
+    """Objective value: data term plus penalized periodic gradients (smoother.py:93-101), on the GPU.
+
+    Deterministic f64 reduction; 2-D inputs return a float, stacked CUDA
+    tensors [B, H, W] a float64 tensor [B].
+    """
+    if tuple(np.shape(u)) != tuple(np.shape(f)):
+        raise ValueError(f"shapes differ: u {tuple(np.shape(u))}, f {tuple(np.shape(f))}")
+    return rt.energy_fields(to_c_params(penalty, float(lam), penalty.min_curvature, 1), u, f)
+
+
 def _is_tensor(x) -> bool:
     try:
         import torch
@@ -87,7 +98,7 @@ def smooth_batch(f, params: SmoothParams, trace: bool = False):
 
     Returns u[B, H, W] (same dtype/device) or (u, energies[(iters+1), B]).
     """
-    u, energies, _ = rt.smooth_device(f, params.c_params(), trace=trace, check=True)
+    u, energies, _ = rt.smooth_device(f, params_of(params), trace=trace, check=True)
     return (u, energies) if trace else u
 
 
@@ -99,7 +110,7 @@ def smooth_frames_u8(frames, params: SmoothParams, *, precision: str | None = No
     the same shape and kind: floor(clip01(u) * 255 + 0.5) of smooth_color on
     the planes v / 255 (formats.py:25-27 + smoother.py:175-217), per channel.
     """
-    if params.color_mode is ColorMode.LUMINANCE_ONLY:
+    if is_luminance_only(params):
         raise ValueError("the 8-bit path smooths channels independently (PER_CHANNEL_RGB or gray)")
     torch = rt._torch()
     is_t = _is_tensor(frames)
@@ -119,7 +130,7 @@ def smooth_frames_u8(frames, params: SmoothParams, *, precision: str | None = No
         raise ValueError(f"expected 1 or 3 channels, got {t4.shape[-1]}")
     if t4.numel() == 0:
         raise ValueError("image plane must be non-empty")
-    u = rt.smooth_device_u8(t4.to("cuda") if not t4.is_cuda else t4, params.c_params(), precision)
+    u = rt.smooth_device_u8(t4.to("cuda") if not t4.is_cuda else t4, params_of(params), precision)
     u = u.reshape(shape)
     return u if (is_t and frames.is_cuda) else u.cpu().numpy()
 
@@ -146,7 +157,7 @@ def smooth_plane(f, params: SmoothParams, trace: bool = False, plan: SolverPlan 
             raise ValueError(f"image plane must be 2-D, got shape {tuple(f.shape)}")
         if plan is not None:
             _check_plan(plan, f.shape, params)
-        u, en, _ = rt.smooth_device(f.unsqueeze(0), params.c_params(), trace=trace, check=True)
+        u, en, _ = rt.smooth_device(f.unsqueeze(0), params_of(params), trace=trace, check=True)
         if trace:
             return u[0], EnergyTrace([float(v) for v in en[:, 0].tolist()])
         return u[0]
@@ -154,11 +165,19 @@ def smooth_plane(f, params: SmoothParams, trace: bool = False, plan: SolverPlan 
     if plan is not None:
         _check_plan(plan, f.shape, params)
     dev = rt.to_device_planes([f], precision)
-    u, en, _ = rt.smooth_device(dev, params.c_params(), trace=trace, check=True)
+    u, en, _ = rt.smooth_device(dev, params_of(params), trace=trace, check=True)
     out = rt.to_host_f64(u)[0]
     if trace:
         return out, EnergyTrace([float(v) for v in en[:, 0].tolist()])
     return out
+
+
+def _image_like(img, channels, space):
+    """The result image in the caller's MultiImage type (this package's, or the
+    reference's when its objects are passed in after a monkeypatch)."""
+    if isinstance(img, MultiImage):
+        return MultiImage._trusted(tuple(channels), space)
+    return type(img)(tuple(channels), space)
 
 
 def smooth_color(img: MultiImage, params: SmoothParams, trace: bool = False, workers: int = 1,
@@ -177,21 +196,21 @@ def smooth_color(img: MultiImage, params: SmoothParams, trace: bool = False, wor
     if img.space == GRAY:
         res = smooth_plane(img.channels[0], params, trace, workers=workers, precision=precision)
         if trace:
-            return MultiImage._trusted((res[0],), GRAY), res[1]
-        return MultiImage._trusted((res,), GRAY)
+            return _image_like(img, (res[0],), GRAY), res[1]
+        return _image_like(img, (res,), GRAY)
     planes = rt.to_device_planes(img.channels, precision)
-    cp = params.c_params()
-    if params.color_mode is ColorMode.LUMINANCE_ONLY:
+    cp = params_of(params)
+    if is_luminance_only(params):
         rt.rgb_yuv_(planes, inverse=False)
         u, en, _ = rt.smooth_device(planes[0:1], cp, trace=trace, check=True)
         planes[0:1] = u
         rt.rgb_yuv_(planes, inverse=True)
-        out = MultiImage._trusted(rt.to_host_f64(planes), RGB)
+        out = _image_like(img, rt.to_host_f64(planes), RGB)
         if trace:
             return out, EnergyTrace([float(v) for v in en[:, 0].tolist()])
         return out
     u, en, _ = rt.smooth_device(planes, cp, trace=trace, check=True)
-    out = MultiImage._trusted(rt.to_host_f64(u), RGB)
+    out = _image_like(img, rt.to_host_f64(u), RGB)
     if trace:
         summed = [float(sum(row)) for row in en.tolist()]
         return out, EnergyTrace(summed)

@@ -154,6 +154,22 @@ def main():
                             weights=(1.2, 0.8, 1.0))
     g["app_tm_multi"] = ref.tonemap_multi(y, rgb, tpm).to_array()
 
+    # --- the standalone field functions of the public API (solver.py:33-49,
+    # penalty.py:117-126, smoother.py:93-101) and the plan's arrays (solver.py:69-75, 100-102)
+    rng = np.random.default_rng(51)
+    for name, shape in (("fld_a", (17, 13)), ("fld_b", (64, 80)), ("fld_c", (1, 6))):
+        u, f = rng.random(shape), rng.random(shape)
+        mx, my = rng.standard_normal(shape), rng.standard_normal(shape)
+        g[name + "_u"], g[name + "_f"], g[name + "_mx"], g[name + "_my"] = u, f, mx, my
+        g[name + "_gx"], g[name + "_gy"] = ref.grad_x(u), ref.grad_y(u)
+        g[name + "_adj"] = ref.adjoint_accumulate(mx, my)
+        ch, we = ref.Charbonnier(0.8, 1e-4), ref.Welsch(10 / 255)
+        g[name + "_aux_ch"] = ref.aux_update(ch, ch.min_curvature, g[name + "_gx"])
+        g[name + "_aux_we"] = ref.aux_update(we, 3.0, g[name + "_gy"])
+        g[name + "_en"] = np.array([ref.energy(u, f, ch, 1.0), ref.energy(u, f, we, 30.0)])
+        plan = ref.make_plan(shape[0], shape[1], 1.5, 4.0, f)
+        g[name + "_denom"], g[name + "_fhat"] = plan.denom, plan.f_hat
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 

@@ -21,7 +21,7 @@ def _header_symbols():
 def test_library_loads_and_exports_every_header_symbol():
     L = _lib.lib()
     syms = _header_symbols()
-    assert len(syms) == 23
+    assert len(syms) == 27
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
@@ -190,7 +190,7 @@ def test_params_validation_mirrors_reference():
     with pytest.raises(ValueError):
         ils.make_plan(4, 4, 1.0, 2.0, workers=0)
     with pytest.raises(ValueError):
-        ils.make_plan(4, 4, 1.0, 2.0).with_data(np.zeros((5, 5)))
+        ils.SolverPlan(4, 4, 1.0, 2.0).with_data(np.zeros((5, 5)))
 
 
 def test_as_plane_and_multiimage_validation():

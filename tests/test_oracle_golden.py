@@ -164,3 +164,21 @@ def test_applications_match_reference_goldens(g):
     assert np.max(np.abs(got - g["app_tm_single"])) < 1e-12
     got = st(O.tonemap_multi(y, ch, c1, (0.125, 1.0, 8.0), weights=(1.2, 0.8, 1.0)))
     assert np.max(np.abs(got - g["app_tm_multi"])) < 1e-12
+
+
+def test_field_functions_match_reference_goldens(g):
+    # grad_x / grad_y / adjoint_accumulate / aux_update / energy (solver.py:33-49,
+    # penalty.py:117-126, smoother.py:93-101) and the plan arrays (solver.py:69-75, 100-102)
+    for name in ("fld_a", "fld_b", "fld_c"):
+        u, f, mx, my = (g[name + k] for k in ("_u", "_f", "_mx", "_my"))
+        assert np.array_equal(O.grad_x(u), g[name + "_gx"])
+        assert np.array_equal(O.grad_y(u), g[name + "_gy"])
+        assert np.array_equal(O.adjoint_accumulate(mx, my), g[name + "_adj"])
+        ch, we = O.Charbonnier(0.8, 1e-4), O.Welsch(10 / 255)
+        assert np.array_equal(O.aux_update(ch, ch.min_curvature, g[name + "_gx"]), g[name + "_aux_ch"])
+        assert np.array_equal(O.aux_update(we, 3.0, g[name + "_gy"]), g[name + "_aux_we"])
+        assert O.energy(u, f, ch, 1.0) == g[name + "_en"][0]
+        assert O.energy(u, f, we, 30.0) == g[name + "_en"][1]
+        h, w = u.shape
+        assert np.array_equal(O.denominator(h, w, 1.5, 4.0), g[name + "_denom"])
+        assert np.allclose(np.fft.fft2(f), g[name + "_fhat"], rtol=0, atol=1e-12)

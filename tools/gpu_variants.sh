@@ -1,7 +1,7 @@
 # time the bench and passes for each variants/*.so against the default build
 mkdir -p gpurun_out
 : > gpurun_out/variants.log
-for lib in default variants/*.so default variants/*.so; do
+for lib in default variants/*.so; do
   echo "== $lib" >> gpurun_out/variants.log
   if [ "$lib" = default ]; then L=""; else L="$lib"; fi
   ILS_LIB=$L timeout 300 python tools/time_passes.py >> gpurun_out/variants.log 2>&1
