@@ -203,6 +203,46 @@ ILS_API ils_status ils_energy(const ils_params* params, const void* u_dev, const
                               int32_t height, int32_t width, int64_t plane_stride, int32_t dtype, double* out_dev,
                               void* scratch, void* stream);
 
+/* tonemap_single / tonemap_multi (applications.py:132-183) on the GPU: log10
+ * of the luminance (+ log_offset), the ILS base smoothing of all scales as
+ * ONE batched launch sequence with a per-plane lambda (plan batch = nscales;
+ * its penalty, c and iters are TonemapParams.base_params', its lam is
+ * replaced by lam[s] per plane), the base compression (_compress_base,
+ * :111-118) and the recolouring (_recolor, :121-129) -- float64 in and out:
+ * lum [H][W], rgb and out [3][H][W].  scalars_dev (3 doubles) receives the
+ * coarsest base's max, its spread (max - min) and target_range / spread; the
+ * caller raises NumericalError when spread < 1e-9 (:113-116).  workspace:
+ * ils_tonemap_workspace_size bytes.  Asynchronous. */
+typedef struct {
+  int32_t nscales;      /* 1 (tonemap_single) or 3 (tonemap_multi, fine to coarse) */
+  double lam[3];        /* base smoothing lambda per scale */
+  double weights[3];    /* detail weights, finest first (multi) */
+  double target_range;  /* > 0 */
+  double saturation;    /* (0, 1] */
+  double log_offset;    /* > 0 */
+} ils_tonemap_params;
+ILS_API ils_status ils_tonemap_workspace_size(const ils_plan* plan, size_t* bytes);
+ILS_API ils_status ils_tonemap(const ils_plan* plan, const double* lum_dev, const double* rgb_dev, double* out_dev,
+                               const ils_tonemap_params* params, void* workspace, void* stream, int32_t* status_dev,
+                               double* scalars_dev);
+
+/* detail_enhance's boost (applications.py:90-92) on n elements: out =
+ * clip01(u + k (f - u)) (ILS_EPI_DETAIL's arithmetic, for planes that did not
+ * come out of ils_smooth_epilogue, e.g. the LUMINANCE_ONLY round trip). */
+ILS_API ils_status ils_detail_boost(const void* f_dev, const void* u_dev, void* out_dev, int64_t n, double k,
+                                    int32_t dtype, void* stream);
+/* Element-wise dtype conversion of n values (round to nearest even): the
+ * drop-in's float64 host planes <-> the fp32 compute planes (as_plane's
+ * float64 contract, image.py:36-45; output fresh float64, solver.py:134). */
+ILS_API ils_status ils_convert(const void* src_dev, int32_t src_dtype, void* dst_dev, int32_t dst_dtype, int64_t n,
+                               void* stream);
+/* SolverPlan.denom (solver.py:100-102) as a float64 height x width array. */
+ILS_API ils_status ils_denominator(double* out_dev, int32_t height, int32_t width, double lam, double c, void* stream);
+/* SolverPlan.f_hat (solver.py:69-75): the full complex128 height x width fft2 of
+ * a real plane from its fp64 half spectrum (rows of spec_pitch >= width/2+1). */
+ILS_API ils_status ils_hermitian_full(const void* half_dev, int64_t spec_pitch, void* full_dev, int32_t height,
+                                      int32_t width, void* stream);
+
 /* ---- C5: one image slab-decomposed over nranks GPUs --------
  * Rank r owns rows [row0[r], row0[r+1]) for the row passes and spectrum
  * columns [col0[r], col0[r+1]) for the column passes.  Between them the
@@ -246,6 +286,10 @@ typedef struct {
   int32_t col2_spec;         /* two-stage column solve kernel id, -1 = k_col */
   int32_t col2_n1, col2_n2;  /* its split H = n1 * n2 */
   int32_t col2_cols;         /* spectrum columns per CTA */
+  int32_t col3_spec;         /* three-stage column solve kernel id (takes precedence), -1 = none */
+  int32_t col3_n1, col3_n2, col3_n3; /* its split H = n1 * n2 * n3 */
+  int32_t col3_cols;         /* spectrum columns per CTA */
+  int32_t row_roll_rows;     /* > 0: rolling-band first / fused row passes, rows per CTA chunk */
 } ils_plan_info;
 ILS_API ils_status ils_plan_get_info(const ils_plan* plan, ils_plan_info* info);
 

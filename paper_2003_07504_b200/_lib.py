@@ -29,6 +29,8 @@ EXPORTS = (
     "ils_slab_col_pass",
     "ils_solve_ls", "ils_rfft2", "ils_irfft2", "ils_rgb_yuv", "ils_plan_get_info", "ils_last_error",
     "ils_abi_version", "ils_grad", "ils_adjoint_accumulate", "ils_aux_update", "ils_energy",
+    "ils_convert", "ils_denominator", "ils_hermitian_full", "ils_tonemap_workspace_size", "ils_tonemap",
+    "ils_detail_boost",
 )
 
 
@@ -39,6 +41,11 @@ class Params(C.Structure):
 
 class HqsParams(C.Structure):
     _fields_ = [("lam", C.c_double), ("beta0", C.c_double), ("kappa", C.c_double), ("iters", C.c_int32)]
+
+
+class TonemapParamsC(C.Structure):
+    _fields_ = [("nscales", C.c_int32), ("lam", C.c_double * 3), ("weights", C.c_double * 3),
+                ("target_range", C.c_double), ("saturation", C.c_double), ("log_offset", C.c_double)]
 
 
 class Epilogue(C.Structure):
@@ -56,7 +63,9 @@ class PlanInfo(C.Structure):
         "row_passes", "col_passes", "row_group", "col_group", "row_spec", "col_spec", "row_swz", "col_swz")] + [
         ("row_radix", C.c_int32 * 16), ("col_radix", C.c_int32 * 16),
         ("spec_pitch", C.c_int64), ("launches_per_call", C.c_int32),
-        ("col2_spec", C.c_int32), ("col2_n1", C.c_int32), ("col2_n2", C.c_int32), ("col2_cols", C.c_int32)]
+        ("col2_spec", C.c_int32), ("col2_n1", C.c_int32), ("col2_n2", C.c_int32), ("col2_cols", C.c_int32),
+        ("col3_spec", C.c_int32), ("col3_n1", C.c_int32), ("col3_n2", C.c_int32), ("col3_n3", C.c_int32),
+        ("col3_cols", C.c_int32), ("row_roll_rows", C.c_int32)]
 
     def as_dict(self):
         d = {n: getattr(self, n) for n, _ in self._fields_ if n not in ("row_radix", "col_radix")}
@@ -101,6 +110,12 @@ _SIGS = {
     "ils_aux_update": (C.c_int, [C.POINTER(Params), _P, _P, C.c_int64, C.c_int32, _P]),
     "ils_energy": (C.c_int, [C.POINTER(Params), _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _P,
                              _P, _P]),
+    "ils_convert": (C.c_int, [_P, C.c_int32, _P, C.c_int32, C.c_int64, _P]),
+    "ils_denominator": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_double, _P]),
+    "ils_hermitian_full": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, _P]),
+    "ils_tonemap_workspace_size": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
+    "ils_tonemap": (C.c_int, [_P, _P, _P, _P, C.POINTER(TonemapParamsC), _P, _P, _P, _P]),
+    "ils_detail_boost": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_int32, _P]),
     "ils_last_error": (C.c_char_p, []),
     "ils_abi_version": (C.c_int32, []),
 }

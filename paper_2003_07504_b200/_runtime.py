@@ -310,7 +310,12 @@ def to_device_planes(planes, precision=None):
     _parallel(lambda i: np.copyto(host[i], arrs[i]), B)
     dev = stage.to("cuda", non_blocking=True)
     _pinned_done("in", torch.cuda.current_stream())
-    return dev if dt == torch.float64 else dev.to(dt)
+    if dt == torch.float64:
+        return dev
+    out = torch.empty((B, H, W), dtype=dt, device=dev.device)  # narrowed by the library's own kernel
+    _lib.check(_lib.lib().ils_convert(C.c_void_p(dev.data_ptr()), _lib.ILS_F64, C.c_void_p(out.data_ptr()),
+                                      _lib.ILS_F32, dev.numel(), _stream_ptr(torch, dev.device)), "ils_convert")
+    return out
 
 
 def to_host_f64(t):
@@ -457,16 +462,11 @@ def energy_fields(cparams, u, f):
 
 def denominator(height, width, lam, c):
     """SolverPlan.denom (solver.py:100-102) as a float64 numpy array, evaluated on the GPU."""
-    import math
-
     torch = _torch()
-    with torch.no_grad():
-        kx = torch.arange(width, dtype=torch.float64, device="cuda")
-        ky = torch.arange(height, dtype=torch.float64, device="cuda")
-        wx = 2.0 - 2.0 * torch.cos(2.0 * math.pi * kx / width)
-        wy = 2.0 - 2.0 * torch.cos(2.0 * math.pi * ky / height)
-        d = 1.0 + (c * lam / 2.0) * (wy[:, None] + wx[None, :])
-    return d.cpu().numpy()
+    out = torch.empty((height, width), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().ils_denominator(C.c_void_p(out.data_ptr()), height, width, float(lam), float(c),
+                                          _stream_ptr(torch, out.device)), "ils_denominator")
+    return out.cpu().numpy()
 
 
 def fft2_full(f):
@@ -478,16 +478,17 @@ def fft2_full(f):
     x = torch.from_numpy(np.ascontiguousarray(np.asarray(f, dtype=np.float64))).to("cuda")
     H, W = x.shape
     try:
-        half = rfft2_device(x[None])[0]  # [H, W//2 + 1]
+        half = rfft2_device(x[None])[0]  # [H, W//2 + 1] view of rows spec_pitch apart
+        pitch = half.stride(0)
     except ValueError:
         # no fp64 plan for this size (fp64 lines stop at about 4096 points):
         # the fp32 transform, widened (relative error ~1e-7)
-        half = rfft2_device(x[None].float())[0].to(torch.complex128)
-    Wc = W // 2 + 1
+        h32 = rfft2_device(x[None].float())[0]
+        pitch = h32.stride(0)
+        half = torch.empty((H, pitch), dtype=torch.complex128, device=x.device)
+        _lib.check(_lib.lib().ils_convert(C.c_void_p(h32.data_ptr()), _lib.ILS_F32, C.c_void_p(half.data_ptr()),
+                                          _lib.ILS_F64, 2 * H * pitch, _stream_ptr(torch, x.device)), "ils_convert")
     full = torch.empty((H, W), dtype=torch.complex128, device=x.device)
-    full[:, :Wc] = half
-    if W > Wc:
-        rows = (-torch.arange(H, device=x.device)) % H
-        cols = W - torch.arange(Wc, W, device=x.device)
-        full[:, Wc:] = half[rows][:, cols].conj()
+    _lib.check(_lib.lib().ils_hermitian_full(C.c_void_p(half.data_ptr()), pitch, C.c_void_p(full.data_ptr()), H, W,
+                                             _stream_ptr(torch, x.device)), "ils_hermitian_full")
     return full.cpu().numpy()

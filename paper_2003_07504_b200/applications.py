@@ -124,9 +124,12 @@ def detail_enhance(img: MultiImage, params: SmoothParams, boost: DetailBoost = D
         # is element-wise on the device in float64
         torch = rt._torch()
         u = smooth_color(img, params, precision=precision)
-        f = torch.tensor(np.stack(img.channels), device="cuda")
-        s = torch.tensor(np.stack(u.channels), device="cuda")
-        out = torch.clamp(s + boost.k * (f - s), 0.0, 1.0)
+        f = torch.from_numpy(np.stack(img.channels)).to("cuda")
+        s = torch.from_numpy(np.stack(u.channels)).to("cuda")
+        out = torch.empty_like(f)
+        _lib.check(_lib.lib().ils_detail_boost(C.c_void_p(f.data_ptr()), C.c_void_p(s.data_ptr()),
+                                               C.c_void_p(out.data_ptr()), f.numel(), float(boost.k), _lib.ILS_F64,
+                                               rt._stream_ptr(torch, f.device)), "ils_detail_boost")
         return _image_out(out, img.space)
     planes = rt.to_device_planes(img.channels, precision)
     return _image_out(_smooth_epilogue(planes, params, boost.k), img.space)
@@ -145,76 +148,54 @@ def _check_hdr_inputs(lum, rgb: MultiImage) -> None:
             raise ValueError("hdr rgb channels must be non-negative")
 
 
-def _compress_base(base, target_range: float):
-    """applications.py:111-118 on a CUDA float64 tensor."""
-    spread = float(base.max() - base.min())
-    if spread < 1e-9:
-        raise NumericalError(f"degenerate base dynamic range {spread:g}; nothing to compress")
-    cf = target_range / spread
-    return (base - base.max()) * cf
-
-
-def _recolor(lum, rgb_planes, log_lum_out, saturation: float) -> MultiImage:
-    """applications.py:121-129 on CUDA float64 tensors."""
-    torch = rt._torch()
-    lum_out = torch.pow(10.0, log_lum_out)
-    out = torch.clamp(torch.pow(rgb_planes / lum, saturation) * lum_out, 0.0, 1.0)
-    return _image_out(out, RGB)
-
-
-def _bases(log_lum64, params_list, precision):
-    """Smooth the log luminance once per parameter set; the sets run concurrently on separate streams."""
-    torch = rt._torch()
-    dt = rt.torch_dtype(precision)
-    f = log_lum64.to(dt)[None]
-    cur = torch.cuda.current_stream()
-    outs = [None] * len(params_list)
-    streams = [torch.cuda.Stream() for _ in params_list]
-    statuses = []
-    for i, (prm, st) in enumerate(zip(params_list, streams)):
-        st.wait_stream(cur)
-        with torch.cuda.stream(st):
-            u, _, status = rt.smooth_device(f, params_of(prm), check=False)
-            outs[i] = u[0]
-            statuses.append(status)
-    for st in streams:
-        cur.wait_stream(st)
-    for u in outs:
-        u.record_stream(cur)
-    for s in statuses:
-        rt.raise_status(int(s.item()))
-    return [u.to(torch.float64) for u in outs]
-
-
-def tonemap_single(hdr_luminance, rgb: MultiImage, tp: TonemapParams, *, precision: str | None = None) -> MultiImage:
-    """applications.py:132-150."""
+def _tonemap(hdr_luminance, rgb: MultiImage, tp: TonemapParams, lambdas, precision) -> MultiImage:
+    """applications.py:132-183 through ils_tonemap: log10 luminance, every scale's base
+    smoothing in one batched launch sequence (a lambda per plane), base compression and
+    recolouring -- all hand-written kernels, float64 in and out."""
     torch = rt._torch()
     lum = as_plane(hdr_luminance)
     _check_hdr_inputs(lum, rgb)
-    lum_d = torch.tensor(lum, device="cuda")
-    log_lum = torch.log10(lum_d + tp.log_offset)
-    (base,) = _bases(log_lum, [tp.base_params], precision)
-    detail = log_lum - base
-    log_lum_out = _compress_base(base, tp.target_range) + detail
-    return _recolor(lum_d, torch.tensor(np.stack(rgb.channels), device="cuda"), log_lum_out, tp.saturation)
+    ns = len(lambdas)
+    prm = tp.base_params
+    code = _lib.ILS_F32 if (precision or rt.get_default_precision()) == "fp32" else _lib.ILS_F64
+    H, W = lum.shape
+    plan = rt.get_plan(ns, H, W, params_of(replace(prm, lam=float(lambdas[-1]))), code, torch.cuda.current_device())
+    c = _lib.TonemapParamsC()
+    c.nscales = ns
+    for k in range(3):
+        c.lam[k] = float(lambdas[min(k, ns - 1)])
+        c.weights[k] = float(tp.weights[k])
+    c.target_range, c.saturation, c.log_offset = float(tp.target_range), float(tp.saturation), float(tp.log_offset)
+    L = _lib.lib()
+    wsz = C.c_size_t()
+    _lib.check(L.ils_tonemap_workspace_size(plan.ptr, C.byref(wsz)), "ils_tonemap_workspace_size")
+    lum_d = torch.from_numpy(np.ascontiguousarray(lum)).to("cuda")
+    rgb_d = torch.from_numpy(np.ascontiguousarray(np.stack(rgb.channels))).to("cuda")
+    out = torch.empty_like(rgb_d)
+    ws = torch.empty(wsz.value, dtype=torch.uint8, device="cuda")
+    status = torch.empty(1, dtype=torch.int32, device="cuda")
+    sc = torch.empty(3, dtype=torch.float64, device="cuda")
+    _lib.check(L.ils_tonemap(plan.ptr, C.c_void_p(lum_d.data_ptr()), C.c_void_p(rgb_d.data_ptr()),
+                             C.c_void_p(out.data_ptr()), C.byref(c), C.c_void_p(ws.data_ptr()),
+                             rt._stream_ptr(torch, lum_d.device), C.c_void_p(status.data_ptr()),
+                             C.c_void_p(sc.data_ptr())), "ils_tonemap")
+    rt.raise_status(int(status.item()))
+    spread = float(sc[1].item())
+    if spread < 1e-9:  # _compress_base, applications.py:112-116
+        raise NumericalError(f"degenerate base dynamic range {spread:g}; nothing to compress")
+    return _image_out(out, RGB)
+
+
+def tonemap_single(hdr_luminance, rgb: MultiImage, tp: TonemapParams, *, precision: str | None = None) -> MultiImage:
+    """applications.py:132-150 (one scale: base, detail, compression, recolouring)."""
+    return _tonemap(hdr_luminance, rgb, tp, (tp.base_params.lam,), precision)
 
 
 def tonemap_multi(hdr_luminance, rgb: MultiImage, tp: TonemapParams, *, precision: str | None = None) -> MultiImage:
     """applications.py:153-183: three scales, coarsest base compressed, details reweighted."""
     if tp.lambdas is None:
         raise ValueError("tonemap_multi needs tp.lambdas (a fine-to-coarse triple)")
-    torch = rt._torch()
-    lum = as_plane(hdr_luminance)
-    _check_hdr_inputs(lum, rgb)
-    lum_d = torch.tensor(lum, device="cuda")
-    log_lum = torch.log10(lum_d + tp.log_offset)
-    b = _bases(log_lum, [replace(tp.base_params, lam=lam) for lam in tp.lambdas], precision)
-    d0 = log_lum - b[0]
-    d1 = b[0] - b[1]
-    d2 = b[1] - b[2]
-    w0, w1, w2 = tp.weights
-    log_lum_out = _compress_base(b[2], tp.target_range) + w2 * d2 + w1 * d1 + w0 * d0
-    return _recolor(lum_d, torch.tensor(np.stack(rgb.channels), device="cuda"), log_lum_out, tp.saturation)
+    return _tonemap(hdr_luminance, rgb, tp, tp.lambdas, precision)
 
 
 def clipart_clean(img: MultiImage, gamma: float, lam: float, *, precision: str | None = None) -> MultiImage:

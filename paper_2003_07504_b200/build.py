@@ -23,12 +23,16 @@ N_COL_SPECS = 6
 UNITS = ([("ils_api.cu", "api", [])]
          + [("ils_inst.cu", f"row_rt_{t}", [f"-DILS_INST_ROW_RT={t}"]) for t in ("float", "double")]
          + [("ils_inst.cu", f"col_rt_{t}", [f"-DILS_INST_COL_RT={t}"]) for t in ("float", "double")]
-         + [("ils_inst.cu", f"row_spec{i}", [f"-DILS_INST_ROW_SPEC={i}"]) for i in range(N_ROW_SPECS)]
+         # compile-time fp32 row plans: FFT butterflies and stencil on the packed FP32x2 pipe
+         + [("ils_inst.cu", f"row_spec{i}", [f"-DILS_INST_ROW_SPEC={i}", "-DILS_PACKED_F32X2"])
+            for i in range(N_ROW_SPECS)]
          + [("ils_inst.cu", f"col_spec{i}", [f"-DILS_INST_COL_SPEC={i}"]) for i in range(N_COL_SPECS)]
-         + [("ils_inst.cu", "col2", ["-DILS_INST_COL2", "-DILS_PACKED_F32X2"])])
+         + [("ils_inst.cu", "col2", ["-DILS_INST_COL2", "-DILS_PACKED_F32X2"])]
+         + [("ils_inst.cu", "col3", ["-DILS_INST_COL3", "-DILS_PACKED_F32X2"])])
 SOURCES = sorted({u[0] for u in UNITS})
-HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_col2.cuh", "ils_elem.cuh", "ils_inst.cu"]
-BASE_HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh"]
+HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_col2.cuh", "ils_col3.cuh", "ils_elem.cuh",
+           "ils_rowroll.cuh", "ils_inst.cu"]
+BASE_HEADERS = ["ils_dft.cuh", "ils_fft.cuh", "ils_kernels.cuh", "ils_rowroll.cuh"]
 
 
 def _unit_deps(src, tag):
@@ -36,6 +40,8 @@ def _unit_deps(src, tag):
     deps = [src] + BASE_HEADERS
     if tag in ("api", "col2"):
         deps.append("ils_col2.cuh")
+    if tag in ("api", "col3"):
+        deps.append("ils_col3.cuh")
     if tag == "api":
         deps.append("ils_elem.cuh")
     deps = [os.path.join(CSRC, d) for d in deps]

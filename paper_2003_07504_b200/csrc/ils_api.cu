@@ -19,6 +19,8 @@
 #include "../../include/ils_b200.h"
 #include "ils_kernels.cuh"
 #include "ils_col2.cuh"
+#include "ils_col3.cuh"
+#include "ils_rowroll.cuh"
 #include "ils_elem.cuh"
 
 using namespace ils;
@@ -137,6 +139,12 @@ struct Col2Host {
 #define ILS_HOST_COL2(ID, N1, N2, CW, MINB) Col2Host{ID, N1, N2, CW},
 const Col2Host kCol2Specs[] = {ILS_COL2_SPECS(ILS_HOST_COL2)};
 #undef ILS_HOST_COL2
+struct Col3Host {
+  int id, n1, n2, n3, cw;
+};
+#define ILS_HOST_COL3(ID, N1, N2, N3, CW, MINB) Col3Host{ID, N1, N2, N3, CW},
+const Col3Host kCol3Specs[] = {ILS_COL3_SPECS(ILS_HOST_COL3)};
+#undef ILS_HOST_COL3
 
 // Shared-memory wavefronts of one transform relative to the conflict-free
 // ideal, for a line layout (identity or XOR swizzle), following exactly the
@@ -278,6 +286,10 @@ struct ils_plan {
   size_t col_smem;
   int row_spec = -1, col_spec = -1;  // compile-time FFT plan ids (-1: runtime plan)
   int col2 = -1;                     // two-stage column solve (ILS_COL2_SPECS id), -1: k_col
+  int col3 = -1;                     // three-stage column solve (ILS_COL3_SPECS id), -1: none (takes precedence)
+  int roll_rows = 0;                 // > 0: F0 / IT row passes by k_row_roll, chunks of this many rows
+  size_t roll_smem = 0;
+  int roll_pf = 0;                   // k_row_roll prefetch depth (one more set of line slots)
   int sms = 148;                     // SMs of the plan's device (waves model)
   FftHost rowf, colf;
   void* d_tables = nullptr;
@@ -332,7 +344,11 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   int LP = std::max(p.rowf.swz ? (p.N + E - 1) / E * E : 0, (line + 1) & ~1);
   if (p.rowf.swz == 3) LP = std::max(LP, (p.N + p.N / 32 + 1) & ~1);  // padded interior layout
   // packing twiddles staged in shared memory, except for kind-3 plans (L1)
+#ifndef ILS_WREAL_SMEM
   const size_t wreal_bytes = (p.packed && p.rowf.swz != 3) ? (size_t)(p.N / 2 + 1) * elt : 0;
+#else
+  const size_t wreal_bytes = p.packed ? (size_t)(p.N / 2 + 1) * elt : 0;
+#endif
   // Band size: minimise (waves x per-CTA work).  A CTA of band b transforms
   // b+2 lines c2r and b lines r2c; k CTAs fit an SM while smem <= 228/k KB
   // and the register budget (kRowBlocksOf) allows them.
@@ -347,7 +363,7 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
 #ifdef ILS_ROW_MINB
     const int reg_cap = ILS_ROW_MINB;
 #else
-    const int reg_cap = p.row_spec >= 0 ? 3 : 2;
+    const int reg_cap = p.row_spec >= 0 ? (p.N >= 3840 ? 1 : 3) : 2;  // kRowBlocksOf
 #endif
     const int per_sm = (int)std::min<size_t>(reg_cap, (228 * 1024) / (smem + 1024));
     const long ctas = (long)p.B * ((p.H + band - 1) / band);
@@ -364,6 +380,40 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   p.row_threads = kRowThreads;
   p.LP = LP;
   p.row_grid = (p.H + p.band - 1) / p.band;
+  // rolling-band first / fused passes for the wide compile-time plans: a ring
+  // of (line groups + 1) slots per CTA, chunks sized for one wave of
+  // resident CTAs (cost ~ waves x (rows + 2 prologue rows) per CTA)
+  p.roll_rows = 0;
+  if (spec && p.row_spec >= 0 && ILS_ROW_SPEC_ROLL(p.row_spec) && p.dtype == ILS_F32 && p.packed && p.W % 8 == 0 &&
+      !env_int("ILS_NO_ROLL", 0)) {
+    const int ng = kRowThreads / spec->G;
+    const int minb = ILS_ROLL_MINB;  // kRollBlocksOf
+    // slots + packing twiddles (whole pairs) + the mu_y row (ils_rowroll.cuh);
+    // the prefetching ring (2 NG + 1 slots) when it still fits minb CTAs per SM
+    auto roll_smem = [&](int pf) {
+      return (size_t)((1 + pf) * ng + 1) * LP * elt + (size_t)((p.N / 2 + 2) & ~1) * elt + (size_t)p.W * sizeof(float);
+    };
+    // (prefetch depth 1 measured no faster at 3840 -- 178.7 vs 176.2 us per
+    // 4K RGB fused pass -- and it halves the resident CTAs at 7680: opt-in)
+    p.roll_pf = env_int("ILS_ROLL_PF", 0) > 0 && (228 * 1024) / (roll_smem(1) + 1024) >= (size_t)minb;
+    const size_t smem = roll_smem(p.roll_pf);
+    const int per_sm = (int)std::min<size_t>(minb, (228 * 1024) / (smem + 1024));
+    if (per_sm >= 1) {
+      const long slots = (long)p.sms * per_sm;
+      double rbest = 1e300;
+      const int forced = env_int("ILS_ROLL_ROWS", 0);
+      for (int R = forced ? 1 : 2; R <= p.H; ++R) {
+        if (forced && R != std::min(forced, p.H)) continue;
+        const long ctas = (long)p.B * ((p.H + R - 1) / R);
+        const double cost = (double)((ctas + slots - 1) / slots) * (R + 2);
+        if (cost < rbest * (1 - 1e-9)) {
+          rbest = cost;
+          p.roll_rows = R;
+        }
+      }
+      p.roll_smem = smem;
+    }
+  }
   return true;
 }
 
@@ -444,6 +494,14 @@ bool choose_col(ils_plan& p, int maxe, size_t elt) {
   if (p.col2 >= 0 && force2 >= 0)
     for (const Col2Host& c : kCol2Specs)
       if (c.id == force2 && c.n1 * c.n2 == p.H) p.col2 = c.id;
+  // the three-stage kernel is opt-in (ILS_COL3_SPEC=id, or -2 for the first
+  // split of H): measured no faster than k_col2 at 1080 rows and slower at
+  // 2160 / 4320, so k_col2 stays the default
+  p.col3 = -1;
+  const int force3 = env_int("ILS_COL3_SPEC", -1);
+  if (p.dtype == ILS_F32 && !env_int("ILS_NO_SPECS", 0) && force3 != -1)
+    for (const Col3Host& c : kCol3Specs)
+      if (c.n1 * c.n2 * c.n3 == p.H && (force3 < 0 ? p.col3 < 0 : c.id == force3)) p.col3 = c.id;
   return true;
 }
 
@@ -556,6 +614,24 @@ cudaError_t launch_row(const ils_plan* p, int mode, RowArgs<T> a, cudaStream_t s
   }
   const dim3 grid(gx, p->B);
   if constexpr (std::is_same<T, float>::value) {
+    // rolling band: plain periodic planes, no trace / 8-bit ingest / soft threshold
+    const bool roll = p->roll_rows > 0 && (mode == MODE_F0 || mode == MODE_IT) && a.wrap == 1 && a.sin_seg.n == 0 &&
+                      a.sout_seg.n == 0 && a.epart == nullptr && a.f8 == nullptr && a.pen.kind != ILS_SOFT;
+    if (roll) {
+      a.band = p->roll_rows;
+      const dim3 rgrid((p->H + p->roll_rows - 1) / p->roll_rows, p->B);
+      switch (p->row_spec) {
+#define ILS_CASE(ID, ...)                                                        \
+  case ID:                                                                       \
+    if constexpr (ILS_ROW_SPEC_ROLL(ID))                                         \
+      return launch_row_roll_impl<RowSpec<ID>::type>(a, rgrid, p->roll_smem, p->roll_pf, s); \
+    break;
+        ILS_ROW_SPECS(ILS_CASE)
+#undef ILS_CASE
+        default:
+          break;
+      }
+    }
     switch (p->row_spec) {
 #define ILS_CASE(ID, ...) \
   case ID:                \
@@ -588,7 +664,24 @@ cudaError_t launch_col2(const ils_plan* p, const ColArgs<T>& a, int planes, cuda
 }
 
 template <typename T>
+cudaError_t launch_col3(const ils_plan* p, const ColArgs<T>& a, int planes, cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value) {
+    switch (p->col3) {
+#define ILS_CASE(ID, N1, N2, N3, CW, MINB) \
+  case ID:                                 \
+    return launch_col3_impl<N1, N2, N3, CW, MINB>(a, planes, s);
+      ILS_COL3_SPECS(ILS_CASE)
+#undef ILS_CASE
+      default:
+        break;
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
 cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
+  if (p->col3 >= 0 && a.mode == COL_SOLVE) return launch_col3<T>(p, a, p->B, s);
   if (p->col2 >= 0 && a.mode == COL_SOLVE) return launch_col2<T>(p, a, p->B, s);
   const dim3 grid(p->col_grid, p->B);
   if constexpr (std::is_same<T, float>::value) {
@@ -611,7 +704,7 @@ cudaError_t launch_col(const ils_plan* p, const ColArgs<T>& a, cudaStream_t s) {
 template <typename T>
 ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, cudaStream_t s, int32_t* status,
                     double* energies, const unsigned char* f8 = nullptr, unsigned char* u8 = nullptr, int ch = 1,
-                    const ils_epilogue* epi = nullptr) {
+                    const ils_epilogue* epi = nullptr, const double* plane_lam = nullptr, int nlam = 0) {
   cx<T>* Sa = static_cast<cx<T>*>(ws);
   cx<T>* Sb = reinterpret_cast<cx<T>*>(static_cast<char*>(ws) + p->spec_bytes);
   double* ep = reinterpret_cast<double*>(static_cast<char*>(ws) + 2 * p->spec_bytes + 256);
@@ -625,6 +718,18 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
   a.u_ps = ps;
   a.u_rp = p->W;
   a.status = status;
+  // per-plane lambda: the values the uniform plan would derive for that lambda
+  // (pen_dev: lam / 2, col_args: c lam / 2), so a plane's result is bitwise
+  // the one of a plan built for its own lambda
+  T cl2_tab[kMaxPlaneLam] = {};
+  if (nlam > 0) {
+    if (nlam > kMaxPlaneLam || energies || p->prm.kind == ILS_SOFT) return fail(ILS_EINVAL, "bad per-plane lambda table");
+    a.nlam = nlam;
+    for (int k = 0; k < nlam; ++k) {
+      a.lam2_tab[k] = T(plane_lam[k] / 2.0);
+      cl2_tab[k] = T(p->prm.c * plane_lam[k] / 2.0);
+    }
+  }
   if (f8) {
     // 8-bit ingest: deinterleave + v/255 into the workspace's planar f, which
     // every row pass (F0 included) then reads as an ordinary fp32 plane
@@ -666,6 +771,10 @@ ils_status smooth_t(const ils_plan* p, const T* f, T* u, int64_t ps, void* ws, c
     if (n > 0) std::swap(cur, nxt);
     ColArgs<T> ca = col_args<T>(p, cur, COL_SOLVE);
     if (hqs) ca.cl2 = T(hqs_beta(p, n));
+    if (nlam > 0) {
+      ca.nlam = nlam;
+      for (int k = 0; k < nlam; ++k) ca.cl2_tab[k] = cl2_tab[k];
+    }
     ILS_CUDA(launch_col<T>(p, ca, s));
   }
   a.iter = iters;
@@ -967,6 +1076,15 @@ ils_status ils_plan_get_info(const ils_plan* p, ils_plan_info* i) {
       i->col2_n1 = c.n1;
       i->col2_n2 = c.n2;
       i->col2_cols = c.cw;
+    }
+  i->row_roll_rows = p->roll_rows;
+  i->col3_spec = p->col3;
+  for (const Col3Host& c : kCol3Specs)
+    if (c.id == p->col3) {
+      i->col3_n1 = c.n1;
+      i->col3_n2 = c.n2;
+      i->col3_n3 = c.n3;
+      i->col3_cols = c.cw;
     }
   return ILS_OK;
 }
@@ -1521,6 +1639,128 @@ ils_status ils_energy(const ils_params* q, const void* u, const void* f, int32_t
   return ILS_OK;
 }
 
+// ------------------------------------------------------------ tone mapping (applications.py:132-183)
+}  // extern "C"
+
+namespace {
+size_t tm_layout(const ils_plan* p, size_t* off_f, size_t* off_u, size_t* off_part) {
+  size_t ws = 0;
+  ils_workspace_size(p, &ws);
+  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
+  const size_t planes = ((size_t)p->B * p->H * p->W * es + 255) & ~size_t(255);
+  *off_f = (ws + 255) & ~size_t(255);
+  *off_u = *off_f + planes;
+  *off_part = *off_u + planes;
+  return *off_part + 2 * 256 * sizeof(double);
+}
+}  // namespace
+
+extern "C" {
+
+ils_status ils_tonemap_workspace_size(const ils_plan* p, size_t* bytes) {
+  if (!p || !bytes) return fail(ILS_EINVAL, "NULL argument");
+  size_t a, b, c;
+  *bytes = tm_layout(p, &a, &b, &c);
+  return ILS_OK;
+}
+
+ils_status ils_tonemap(const ils_plan* p, const double* lum, const double* rgb, double* out,
+                       const ils_tonemap_params* tp, void* ws, void* stream, int32_t* status, double* sc) {
+  if (!p || !lum || !rgb || !out || !tp || !ws || !status || !sc) return fail(ILS_EINVAL, "NULL argument");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (p->slab || p->prm.kind == ILS_SOFT) return fail(ILS_EINVAL, "tone mapping needs an ILS plan");
+  if (tp->nscales != 1 && tp->nscales != 3) return fail(ILS_EINVAL, "nscales must be 1 or 3, got %d", tp->nscales);
+  if (p->B != tp->nscales) return fail(ILS_EINVAL, "plan batch %d != nscales %d", p->B, tp->nscales);
+  // TonemapParams.__post_init__ (applications.py:53-77)
+  if (!(tp->target_range > 0.0 && std::isfinite(tp->target_range)))
+    return fail(ILS_EINVAL, "target_range must be finite and positive, got %g", tp->target_range);
+  if (!(tp->saturation > 0.0 && tp->saturation <= 1.0)) return fail(ILS_EINVAL, "saturation must be in (0,1], got %g", tp->saturation);
+  if (!(tp->log_offset > 0.0 && std::isfinite(tp->log_offset)))
+    return fail(ILS_EINVAL, "log_offset must be finite and positive, got %g", tp->log_offset);
+  for (int k = 0; k < tp->nscales; ++k)
+    if (!(tp->lam[k] > 0.0 && std::isfinite(tp->lam[k]))) return fail(ILS_EINVAL, "lambdas must be finite and positive");
+  DeviceGuard dg(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  size_t off_f, off_u, off_part;
+  tm_layout(p, &off_f, &off_u, &off_part);
+  char* w = static_cast<char*>(ws);
+  double* part = reinterpret_cast<double*>(w + off_part);
+  const long long npx = (long long)p->H * p->W;
+  const int blocks = elem_blocks(npx);
+  const int mblocks = std::min(256, blocks);
+  auto run = [&](auto tag) -> ils_status {
+    using T = decltype(tag);
+    T* f = reinterpret_cast<T*>(w + off_f);
+    T* u = reinterpret_cast<T*>(w + off_u);
+    k_tm_log<T><<<blocks, 256, 0, s>>>(lum, f, npx, p->B, tp->log_offset);
+    ILS_CUDA(cudaGetLastError());
+    // all scales in one launch sequence, each plane with its own lambda
+    ils_status st = smooth_t<T>(p, f, u, npx, ws, s, status, nullptr, nullptr, nullptr, 1, nullptr, tp->lam,
+                                tp->nscales);
+    if (st != ILS_OK) return st;
+    k_tm_minmax<T><<<mblocks, 256, 0, s>>>(u + (size_t)(p->B - 1) * npx, npx, part);
+    k_tm_minmax_fin<<<1, 32, 0, s>>>(part, mblocks, tp->target_range, sc);
+    k_tm_finish<T><<<blocks, 256, 0, s>>>(lum, rgb, u, p->B, npx, tp->log_offset, tp->weights[0], tp->weights[1],
+                                          tp->weights[2], tp->saturation, sc, out);
+    ILS_CUDA(cudaGetLastError());
+    return ILS_OK;
+  };
+  return p->dtype == ILS_F32 ? run(float{}) : run(double{});
+}
+
+ils_status ils_detail_boost(const void* f, const void* u, void* out, int64_t n, double k, int32_t dtype, void* stream) {
+  if (!f || !u || !out || n < 0) return fail(ILS_EINVAL, "bad detail_boost arguments");
+  if (!(k >= 0.0 && std::isfinite(k))) return fail(ILS_EINVAL, "boost k must be finite and >= 0, got %g", k);
+  if (dtype != ILS_F32 && dtype != ILS_F64) return fail(ILS_EINVAL, "unknown dtype %d", dtype);
+  if (n == 0) return ILS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == ILS_F32)
+    k_detail_boost<float><<<elem_blocks(n), 256, 0, s>>>(static_cast<const float*>(f), static_cast<const float*>(u),
+                                                        static_cast<float*>(out), n, float(k));
+  else
+    k_detail_boost<double><<<elem_blocks(n), 256, 0, s>>>(static_cast<const double*>(f),
+                                                         static_cast<const double*>(u), static_cast<double*>(out), n, k);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+ils_status ils_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n, void* stream) {
+  if (!src || !dst || n < 0) return fail(ILS_EINVAL, "bad convert arguments");
+  if ((src_dtype != ILS_F32 && src_dtype != ILS_F64) || (dst_dtype != ILS_F32 && dst_dtype != ILS_F64))
+    return fail(ILS_EINVAL, "unknown dtype");
+  if (n == 0) return ILS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int blocks = elem_blocks(n);
+  if (src_dtype == ILS_F64 && dst_dtype == ILS_F32)
+    k_convert<double, float><<<blocks, 256, 0, s>>>(static_cast<const double*>(src), static_cast<float*>(dst), n);
+  else if (src_dtype == ILS_F32 && dst_dtype == ILS_F64)
+    k_convert<float, double><<<blocks, 256, 0, s>>>(static_cast<const float*>(src), static_cast<double*>(dst), n);
+  else if (src_dtype == ILS_F32)
+    k_convert<float, float><<<blocks, 256, 0, s>>>(static_cast<const float*>(src), static_cast<float*>(dst), n);
+  else
+    k_convert<double, double><<<blocks, 256, 0, s>>>(static_cast<const double*>(src), static_cast<double*>(dst), n);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+ils_status ils_denominator(double* out, int32_t height, int32_t width, double lam, double c, void* stream) {
+  if (!out || height < 1 || width < 1) return fail(ILS_EINVAL, "bad denominator arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_denom<<<elem_blocks((long long)height * width), 256, 0, s>>>(out, height, width, c * lam / 2.0);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
+ils_status ils_hermitian_full(const void* half, int64_t pitch, void* full, int32_t height, int32_t width,
+                              void* stream) {
+  if (!half || !full || height < 1 || width < 1 || pitch < width / 2 + 1) return fail(ILS_EINVAL, "bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_hermitian_full<<<elem_blocks((long long)height * width), 256, 0, s>>>(
+      static_cast<const cx<double>*>(half), pitch, static_cast<cx<double>*>(full), height, width);
+  ILS_CUDA(cudaGetLastError());
+  return ILS_OK;
+}
+
 // ------------------------------------------------------------ slab decomposition (C5)
 ils_status ils_slab_plan_create(ils_plan** out, int32_t height, int32_t width, const ils_params* params,
                                 int32_t dtype, int32_t device, int32_t nranks, int32_t rank) {
@@ -1681,6 +1921,11 @@ ils_status slab_col_t(const ils_plan* p, cx<T>* recv, cx<T>* send, cudaStream_t 
   c.dst = send;
   const dim3 grid(p->col_grid, 1);
   cudaError_t e;
+  if (p->col3 >= 0) {
+    e = launch_col3<T>(p, c, 1, s);
+    if (e != cudaSuccess) return fail(ILS_ECUDA, "slab col pass: %s", cudaGetErrorString(e));
+    return ILS_OK;
+  }
   if (p->col2 >= 0) {
     e = launch_col2<T>(p, c, 1, s);
     if (e != cudaSuccess) return fail(ILS_ECUDA, "slab col pass: %s", cudaGetErrorString(e));

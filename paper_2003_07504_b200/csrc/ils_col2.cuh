@@ -90,9 +90,10 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
     dft<N2, -1>(w);
     // / denom (solver.py:100-102, 130) with the 1/(H W) of both inverses:
     // the same expression as k_col's DenomScale, so the scale is bit-identical
-    const float base = 1.f + A.cl2 * __ldg(A.wx + min(c0 + c, A.Wc - 1));
+    const float cl2 = A.cl2_of(b);
+    const float base = 1.f + cl2 * __ldg(A.wx + min(c0 + c, A.Wc - 1));
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) w[k2] = scale(w[k2], fast_div(A.inv_hw, base + A.cl2 * swy[r + N1 * k2]));
+    for (int k2 = 0; k2 < N2; ++k2) w[k2] = scale(w[k2], fast_div(A.inv_hw, base + cl2 * swy[r + N1 * k2]));
     dft<N2, +1>(w);
     d[0] = w[0];
 #pragma unroll

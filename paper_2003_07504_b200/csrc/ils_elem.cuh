@@ -133,4 +133,130 @@ __global__ void k_energy_fin(const double* __restrict__ part, int nblk, double l
   if (threadIdx.x == 0) out[blockIdx.x] = s[0] + lam * (s[1] + s[2]);
 }
 
+// dtype conversion of the drop-in's host planes (float64 numpy planes <->
+// the fp32 compute planes): round to nearest even, as numpy's astype
+template <typename S, typename D>
+__global__ void k_convert(const S* __restrict__ src, D* __restrict__ dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = D(src[i]);
+}
+
+// SolverPlan.denom (solver.py:100-102): 1 + (c lam / 2) (wy[r] + wx[x]),
+// w = 2 - 2 cos(2 pi k / n), in float64
+__global__ void k_denom(double* __restrict__ out, int H, int W, double cl2) {
+  const long long n = (long long)H * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / W), x = (int)(i - (long long)r * W);
+    const double wx = 2.0 - 2.0 * cospi(2.0 * x / W);
+    const double wy = 2.0 - 2.0 * cospi(2.0 * r / H);
+    out[i] = __dadd_rn(1.0, __dmul_rn(cl2, wy + wx));  // numpy's roundings, no contraction
+  }
+}
+
+// fft2 of real data (SolverPlan.f_hat, solver.py:69-75) from its half
+// spectrum: X[k1][k2] = half[k1][k2] for k2 <= W/2, else conj(half[-k1 mod H][W - k2])
+__global__ void k_hermitian_full(const cx<double>* __restrict__ half, long long pitch, cx<double>* __restrict__ full,
+                                 int H, int W) {
+  const long long n = (long long)H * W;
+  const int wc = W / 2 + 1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int k1 = (int)(i / W), k2 = (int)(i - (long long)k1 * W);
+    if (k2 < wc) {
+      full[i] = half[(long long)k1 * pitch + k2];
+    } else {
+      const cx<double> v = half[(long long)(k1 == 0 ? 0 : H - k1) * pitch + (W - k2)];
+      full[i] = cx<double>{v.x, -v.y};
+    }
+  }
+}
+
+// detail_enhance's boost (applications.py:90-92) on given planes: clip01(u + k (f - u))
+template <typename T>
+__global__ void k_detail_boost(const T* __restrict__ f, const T* __restrict__ u, T* __restrict__ out, long long n,
+                               T k) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = detail_epilogue(u[i], f[i], k);
+}
+
+// ------------------------------------------------------------ tone mapping (applications.py:111-183)
+// log10 luminance (:143, :166) narrowed to the compute type, one copy per scale plane
+template <typename T>
+__global__ void k_tm_log(const double* __restrict__ lum, T* __restrict__ f, long long npx, int nplanes, double off) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npx; i += (long long)gridDim.x * blockDim.x) {
+    const T v = T(log10(__dadd_rn(lum[i], off)));
+    for (int s = 0; s < nplanes; ++s) f[(size_t)s * npx + i] = v;
+  }
+}
+
+// min / max of the coarsest base (_compress_base, :111-118): per-block partials ...
+template <typename T>
+__global__ void k_tm_minmax(const T* __restrict__ base, long long npx, double* __restrict__ part) {
+  __shared__ double smin[32], smax[32];
+  double lo = INFINITY, hi = -INFINITY;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npx; i += (long long)gridDim.x * blockDim.x) {
+    const double v = double(base[i]);
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smin[threadIdx.x >> 5] = lo;
+    smax[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = fmin(lo, smin[w]);
+      hi = fmax(hi, smax[w]);
+    }
+    part[2 * blockIdx.x] = lo;
+    part[2 * blockIdx.x + 1] = hi;
+  }
+}
+// ... and the scalars: sc[0] = max, sc[1] = spread = max - min, sc[2] = cf = target / spread
+__global__ void k_tm_minmax_fin(const double* __restrict__ part, int nblk, double target, double* __restrict__ sc) {
+  if (threadIdx.x != 0) return;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int i = 0; i < nblk; ++i) {
+    lo = fmin(lo, part[2 * i]);
+    hi = fmax(hi, part[2 * i + 1]);
+  }
+  const double spread = hi - lo;
+  sc[0] = hi;
+  sc[1] = spread;
+  sc[2] = target / spread;
+}
+
+// log_lum_out (:145-147 single, :175-180 multi, left to right as numpy) ->
+// _recolor (:121-129): clip01((C / lum)**saturation * 10**log_lum_out), float64
+template <typename T>
+__global__ void k_tm_finish(const double* __restrict__ lum, const double* __restrict__ rgb, const T* __restrict__ bases,
+                            int nscales, long long npx, double off, double w0, double w1, double w2, double sat,
+                            const double* __restrict__ sc, double* __restrict__ out) {
+  const double mx = sc[0], cf = sc[2];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npx; i += (long long)gridDim.x * blockDim.x) {
+    const double l = lum[i];
+    const double ll = log10(__dadd_rn(l, off));
+    double lo;
+    if (nscales == 1) {
+      const double b = double(bases[i]);
+      lo = __dadd_rn(__dmul_rn(__dsub_rn(b, mx), cf), __dsub_rn(ll, b));
+    } else {
+      const double b0 = double(bases[i]), b1 = double(bases[npx + i]), b2 = double(bases[2 * npx + i]);
+      lo = __dmul_rn(__dsub_rn(b2, mx), cf);
+      lo = __dadd_rn(lo, __dmul_rn(w2, __dsub_rn(b1, b2)));
+      lo = __dadd_rn(lo, __dmul_rn(w1, __dsub_rn(b0, b1)));
+      lo = __dadd_rn(lo, __dmul_rn(w0, __dsub_rn(ll, b0)));
+    }
+    const double lum_out = pow(10.0, lo);
+    for (int c = 0; c < 3; ++c) {
+      const double v = __dmul_rn(pow(__ddiv_rn(rgb[(size_t)c * npx + i], l), sat), lum_out);
+      out[(size_t)c * npx + i] = fmin(fmax(v, 0.0), 1.0);
+    }
+  }
+}
+
 }  // namespace ils

@@ -57,6 +57,7 @@ struct PenaltyDev {
 };
 
 constexpr int kMaxSeg = 8;  // ranks of a slab-decomposed (distributed) transform
+constexpr int kMaxPlaneLam = 4;  // planes of a launch with their own lambda
 
 // Spectrum rows split into column segments: the row-pass side of the
 // distributed FFT transpose.  Segment q holds columns
@@ -108,6 +109,10 @@ struct RowArgs {
   // (detail_enhance, :80-93; k = 0 is the clip01 of clipart/texture presets)
   int epi;
   T epi_k;
+  // per-plane lambda (tonemap_multi's three scales in one batched launch,
+  // applications.py:165-168): nlam > 0 replaces pen.lam2 by lam2_tab[min(b, nlam-1)]
+  int nlam;
+  T lam2_tab[kMaxPlaneLam];
 };
 
 template <typename T>
@@ -130,6 +135,9 @@ struct ColArgs {
   T inv_hw;     // 1 / (H W)
   int mode;
   FftDev<T> fft;
+  int nlam;                   // > 0: plane b uses cl2_tab[min(b, nlam-1)] (see RowArgs::nlam)
+  T cl2_tab[kMaxPlaneLam];
+  __device__ __forceinline__ T cl2_of(int b) const { return nlam > 0 ? cl2_tab[min(b, nlam - 1)] : cl2; }
 };
 
 // ------------------------------------------------------------ penalty math
@@ -170,6 +178,18 @@ __device__ __forceinline__ T aux(T x, const PenaltyDev<T>& P) {
   if constexpr (SOFT) v = fmax(v, P.floor);
   return mul_rn(x, v);
 }
+#if ILS_F32X2
+// aux on two columns at once on the packed FP32x2 pipe: each lane performs
+// exactly aux<false>'s roundings, so results are bitwise the scalar ones
+__device__ __forceinline__ float2 aux2(float2 x, const PenaltyDev<float>& P) {
+  const float2 q = __ffma2_rn(x, x, make_float2(P.eps0, P.eps0));
+  const float2 lg = P.kind != 1 ? make_float2(lg2_(q.x), lg2_(q.y)) : q;
+  const float2 m = __fmul2_rn(make_float2(P.E, P.E), lg);
+  const float2 t = make_float2(ex2_(m.x), ex2_(m.y));
+  const float2 v = __ffma2_rn(make_float2(P.coef, P.coef), t, make_float2(P.c, P.c));
+  return __fmul2_rn(x, v);
+}
+#endif
 // phi(x): penalty.py:60-62, 88-91 (energy trace only)
 template <typename T>
 __device__ __forceinline__ T phi(T x, const PenaltyDev<T>& P) {
@@ -340,30 +360,50 @@ __device__ __forceinline__ void bulk_wait_reads() {
 }
 
 // ------------------------------------------------------------ real <-> half-complex packing
-// packing twiddle k: from the shared-memory copy (SMEM), or -- plans whose
-// padded lines leave no room for it (layout kind 3) -- read-only global
-// memory through L1
+// Packing twiddles w^k = exp(-2 pi i k / W) for the loops below, which visit
+// k = rank + size * m:
+//   TwTab<SMEM>  the host table, staged in shared memory (SMEM) or read
+//                through L1 from global memory
+//   TwSplit      w^rank (a register, loaded once) * w^(32 m) (a 16-entry
+//                shared table): the 32-thread-group plans whose padded line
+//                layout leaves no room for the full table; one complex
+//                multiply (about 2 ulp) instead of an L2 load per twiddle
 template <bool SMEM, typename T>
 __device__ __forceinline__ cx<T> ldw(const cx<T>* w, int k) {
   if constexpr (SMEM) return w[k];
   else return ldg_cx(w + k);
 }
+template <typename T, bool SMEM>
+struct TwTab {
+  const cx<T>* w;
+  __device__ __forceinline__ cx<T> operator()(int k, int) const { return ldw<SMEM>(w, k); }
+};
+template <typename T>
+struct TwSplit {
+  cx<T> lo;         // w^rank
+  const cx<T>* hi;  // hi[m] = w^(32 m), shared memory
+  __device__ __forceinline__ cx<T> operator()(int, int m) const { return cmul(lo, hi[m]); }
+};
+constexpr int kTwSplitMax = 32;  // entries of the w^(32 m) table (N/2 < 32 * 32)
+
 // Forward post-process of one packed line: Z = FFT_N(x[2n] + i x[2n+1]) ->
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
 // O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
-template <typename T, bool SMEM, class Grp>
-__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* wreal, const Grp& g) {
-  for (int k = g.rank; k <= N / 2; k += g.size()) {
+// (complex operations: the packed FP32x2 forms in fp32 translation units)
+template <typename T, class TW, class Grp>
+__device__ __forceinline__ void r2c_post(cx<T>* z, int N, const TW& tw, const Grp& g) {
+  int m = 0;
+  for (int k = g.rank; k <= N / 2; k += g.size(), ++m) {
     if (k == 0) {
       const cx<T> z0 = z[0];
       z[0] = cx<T>{z0.x + z0.y, T(0)};
       z[N] = cx<T>{z0.x - z0.y, T(0)};
     } else {
       const cx<T> zk = z[k], zm = z[N - k];
-      const cx<T> E{T(0.5) * (zk.x + zm.x), T(0.5) * (zk.y - zm.y)};
-      const cx<T> d{T(0.5) * (zk.x - zm.x), T(0.5) * (zk.y + zm.y)};  // (zk - conj zm)/2
-      const cx<T> O{d.y, -d.x};                                          // -i * d
-      const cx<T> wO = cmul(ldw<SMEM>(wreal, k), O);
+      const cx<T> E = scale(zk + conj(zm), T(0.5));
+      const cx<T> d = scale(zk - conj(zm), T(0.5));  // (zk - conj zm)/2
+      const cx<T> O{d.y, -d.x};                      // -i * d
+      const cx<T> wO = cmul(tw(k, m), O);
       z[k] = E + wO;
       if (N - k != k) z[N - k] = conj(E - wO);
     }
@@ -374,19 +414,20 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const cx<T>* wreal, co
 // Inverse pre-process: Z_k = E + iO, Z_{N-k} = conj(E) + i conj(O) with
 // E = X_k + conj X_{N-k}, O = (X_k - conj X_{N-k}) conj(w^k).  An inverse
 // N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
-template <typename T, bool SMEM, class Grp>
-__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const cx<T>* wreal, const Grp& g) {
-  for (int k = g.rank; k <= N / 2; k += g.size()) {
+template <typename T, class TW, class Grp>
+__device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const TW& tw, const Grp& g) {
+  int m = 0;
+  for (int k = g.rank; k <= N / 2; k += g.size(), ++m) {
     if (k == 0) {
       const T a = z[0].x, c = z[N].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
       z[0] = cx<T>{a + c, a - c};
     } else {
       const cx<T> xk = z[k], xm = z[N - k];
-      const cx<T> E{xk.x + xm.x, xk.y - xm.y};
-      const cx<T> D{xk.x - xm.x, xk.y + xm.y};
-      const cx<T> O = cmulc(D, ldw<SMEM>(wreal, k));
-      z[k] = cx<T>{E.x - O.y, E.y + O.x};
-      if (N - k != k) z[N - k] = cx<T>{E.x + O.y, -E.y + O.x};
+      const cx<T> E = xk + conj(xm);
+      const cx<T> D = xk - conj(xm);
+      const cx<T> O = cmulc(D, tw(k, m));
+      z[k] = E + cx<T>{-O.y, O.x};
+      if (N - k != k) z[N - k] = conj(E) + cx<T>{O.y, O.x};
     }
   }
   g.sync();
@@ -420,8 +461,11 @@ constexpr bool kBulkRows = sizeof(T) == 4 && FS::n > 0 && (2 * FS::n) % 8 == 0;
 // than the band-12 CTA's lower halo overhead (4993 -> 5859 frames/s);
 // runtime plans for 2
 #ifndef ILS_ROW_MINB  // (tuning override: resident row CTAs per SM the registers are budgeted for)
+// (the 3840-point line plan -- 7680-wide rows -- fits one CTA per SM in
+// shared memory, so it gets the whole register file: 1.1 KB of spills per
+// thread at 80 registers, IT pass 1285 -> 751 us)
 template <class FS>
-constexpr int kRowBlocksOf = FS::n > 0 ? 3 : 2;
+constexpr int kRowBlocksOf = FS::n > 0 ? (FS::n >= 3840 ? 1 : 3) : 2;
 #else
 template <class FS>
 constexpr int kRowBlocksOf = ILS_ROW_MINB;
@@ -504,17 +548,34 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
   const int off = halo ? 1 : 0;
   const Lines<T, PACKED> L{reinterpret_cast<cx<T>*>(smem_raw), A.LP};
   const PenaltyDev<T>& P = A.pen;
+  const T lam2 = A.nlam > 0 ? A.lam2_tab[min(b, A.nlam - 1)] : P.lam2;  // block-uniform
   const T* fpl = A.f ? A.f + (size_t)b * A.f_ps : nullptr;
   // real-packing twiddles staged in shared memory after the band's lines
-  constexpr bool WSMEM = FS::swz != 3;  // kind-3 plans read them from global memory
+#ifndef ILS_WREAL_SMEM  // kind-3 plans read the packing twiddles from global memory through L1
+  constexpr bool WSMEM = FS::swz != 3;
+#else  // (tuning: a shared-memory table for every plan -- faster passes alone, but the
+       // 4 KB larger row CTAs co-reside worse with the column pass: bench 5879 -> 5353)
+  constexpr bool WSMEM = true;
+#endif
   // (after the band's line slots: band + 2 with halo rows, band without --
   // the final pass runs a band 2 rows taller in the same shared memory)
   cx<T>* swreal = WSMEM ? reinterpret_cast<cx<T>*>(smem_raw) + (size_t)(A.band + (halo ? 2 : 0)) * A.LP
                         : const_cast<cx<T>*>(A.wreal);
+  // kind-3 plans without the table in shared memory: split twiddles
+  constexpr bool WSPLIT = !WSMEM && FS::G == 32 && FS::n / 2 / 32 < kTwSplitMax;
+  __shared__ cx<T> s_whi[WSPLIT ? kTwSplitMax : 1];
   if (PACKED && WSMEM) {
     for (int k = tid; k <= A.N / 2; k += nthr) swreal[k] = A.wreal[k];
     __syncthreads();
   }
+  if (PACKED && WSPLIT) {
+    if (tid * 32 <= A.N / 2) s_whi[tid] = A.wreal[32 * tid];
+    __syncthreads();
+  }
+  using TwT = std::conditional_t<WSPLIT, TwSplit<T>, TwTab<T, WSMEM>>;
+  TwT twp;
+  if constexpr (WSPLIT) twp = TwSplit<T>{ldg_cx(A.wreal + (tid % 32)), s_whi};
+  else twp = TwTab<T, WSMEM>{swreal};
   TwCache<T, FS> twc;
   fill_twcache(twc, A.fft, g);
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
@@ -548,7 +609,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           const T myu = my[(size_t)wrapi(r - 1, H) * A.f_rp + x];
           bx |= !finite_(mxc);
           by |= !finite_(myc);
-          v = v + P.lam2 * ((mxl - mxc) + (myu - myc));
+          v = v + lam2 * ((mxl - mxc) + (myu - myc));
         }
         L.set(i, x, v);
       }
@@ -675,7 +736,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
         if (PACKED) {
-          c2r_pre<T, WSMEM>(z, A.N, swreal, g);
+          c2r_pre<T>(z, A.N, twp, g);
         } else {
           // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
           for (int k = A.Wc + g.rank; k < W; k += g.size()) z[k] = conj(z[W - k]);
@@ -824,6 +885,9 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     double e = 0.0;
     auto band = [&](auto trace_tag) {
       constexpr bool TR = decltype(trace_tag)::value;
+      // packed FP32x2 stencil (column pairs) for whole-strip fp32 plans
+      constexpr bool PKS = ILS_F32X2 && std::is_same<T, float>::value && !TR && !SOFTOK && ALLFULL;
+      float2 chk2 = make_float2(0.f, 0.f);
       T myup[GMAX][QW];
       T fcur[GMAX][QW];
 #pragma unroll
@@ -875,6 +939,39 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
               }
               T mxp = aux<SOFTOK>(uc[0] - L.get(i, wrapi(x0 - 1, W)), P);
               const T uright = L.get(i, wrapi(full ? x0 + QW : min(x0 + QW, W), W));
+#if ILS_F32X2
+              if constexpr (PKS) {
+                // the scalar loop below, two columns per instruction
+                float gxs[QW], mx[QW], my[QW];
+#pragma unroll
+                for (int q = 0; q < QW; ++q) gxs[q] = (q + 1 < QW ? uc[q + 1] : uright) - uc[q];
+#pragma unroll
+                for (int p2 = 0; p2 < QW; p2 += 2) {
+                  const float2 gy2 = __fadd2_rn(make_float2(ud[p2], ud[p2 + 1]), make_float2(-uc[p2], -uc[p2 + 1]));
+                  const float2 m = aux2(make_float2(gxs[p2], gxs[p2 + 1]), P);
+                  const float2 n = aux2(gy2, P);
+                  mx[p2] = m.x;
+                  mx[p2 + 1] = m.y;
+                  my[p2] = n.x;
+                  my[p2 + 1] = n.y;
+                }
+#pragma unroll
+                for (int p2 = 0; p2 < QW; p2 += 2) {
+                  const float ax0 = (p2 == 0 ? mxp : mx[p2 - 1]) - mx[p2], ax1 = mx[p2] - mx[p2 + 1];
+                  const float2 ay = __fadd2_rn(make_float2(myup[gi][p2], myup[gi][p2 + 1]),
+                                               make_float2(-my[p2], -my[p2 + 1]));
+                  const float2 a = __fadd2_rn(make_float2(ax0, ax1), ay);
+                  const float2 l2 = make_float2(lam2, lam2);
+                  const float2 r = is_it ? __fmul2_rn(l2, a) : __ffma2_rn(l2, a, make_float2(uc[p2], uc[p2 + 1]));
+                  rhs[kk][gi][p2] = r.x;
+                  rhs[kk][gi][p2 + 1] = r.y;
+                  chk2 = __ffma2_rn(make_float2(uc[p2], uc[p2 + 1]), make_float2(0.f, 0.f), chk2);
+                }
+#pragma unroll
+                for (int q = 0; q < QW; ++q) myup[gi][q] = my[q];
+                continue;
+              }
+#endif
 #pragma unroll
               for (int q = 0; q < QW; ++q) {
                 if (full || x0 + q < W) {
@@ -888,7 +985,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
                   // r2c's first pass loads each element (phase C), off the
                   // stencil's critical path
                   const T fv = is_it ? fcur[gi][q] : uc[q];
-                  rhs[kk][gi][q] = is_it ? mul_rn(P.lam2, a) : fma_rn(P.lam2, a, fv);
+                  rhs[kk][gi][q] = is_it ? mul_rn(lam2, a) : fma_rn(lam2, a, fv);
                   chk = fma_rn(uc[q], T(0), chk);
                   if constexpr (TR) {
                     const T d = uc[q] - fv;
@@ -928,6 +1025,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           }
         }
       }
+      chk = chk + (chk2.x + chk2.y);  // 0, or NaN when a packed lane saw a non-finite u
     };
     if (trace) band(std::true_type{});
     else band(std::false_type{});
@@ -959,7 +1057,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
       }
       fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
     }
-    if (PACKED) r2c_post<T, WSMEM>(z, A.N, swreal, g);
+    if (PACKED) r2c_post<T>(z, A.N, twp, g);
     else g.sync();
     if (A.sout_seg.n == 0) {
       cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;
@@ -1047,8 +1145,9 @@ __global__ void __launch_bounds__(kColThreadsOf<FS>, kColLaunchBlocksOf<FS>) k_c
     if (A.mode == COL_SOLVE) {
       // / denom (solver.py:100-102, 130) and the 1/(H W) of both inverses,
       // applied as the inverse transform's first pass loads each element
-      const T base = T(1) + A.cl2 * __ldg(A.wx + c0 + c);
-      const DenomScale<T> pre{swy, base, A.cl2, A.inv_hw};
+      const T cl2 = A.cl2_of(b);
+      const T base = T(1) + cl2 * __ldg(A.wx + c0 + c);
+      const DenomScale<T> pre{swy, base, cl2, A.inv_hw};
       fft_line<T, +1, FS>(z, A.fft, g, pre, &twc);
     } else if (A.mode == COL_INV) {
       const UniformScale<T> pre{A.inv_hw};
@@ -1211,6 +1310,9 @@ __global__ void k_gauss_rows(const T* __restrict__ x, T* __restrict__ y, int W, 
 // these radix lists when n matches, so twiddle tables and kernels agree.
 // X(id, swizzle, group threads, elements per thread, n, radices...)
 #define ILS_ROW_SPECS(X) X(0, 1, 32, 16, 256, 16, 16) X(1, 3, 32, 32, 960, 32, 30) X(2, 1, 128, 16, 1920, 16, 15, 8) X(3, 1, 256, 16, 3840, 16, 16, 15) X(4, 1, 32, 16, 512, 16, 8, 4)
+// row specs with a rolling-band first / fused pass (ils_rowroll.cuh): the wide
+// rows (3840, 7680) whose halo lines cost 40% of k_row's inverse transforms
+#define ILS_ROW_SPEC_ROLL(ID) ((ID) == 2 || (ID) == 3)
 // row specs whose width 2n exceeds 4 * kRowThreads * 4 need the WIDE stencil (8-column strips)
 #ifndef ILS_ROW_SPEC_WIDE  // (tuning override: which row specs use 8-column stencil strips)
 #define ILS_ROW_SPEC_WIDE(ID) ((ID) == 3)

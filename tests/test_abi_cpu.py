@@ -21,7 +21,7 @@ def _header_symbols():
 def test_library_loads_and_exports_every_header_symbol():
     L = _lib.lib()
     syms = _header_symbols()
-    assert len(syms) == 27
+    assert len(syms) == 33
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
@@ -88,10 +88,11 @@ def test_column_solve_kernel_choice(h, w, n1n2):
     _lib.lib().ils_plan_get_info(p, C.byref(info))
     d = info.as_dict()
     if n1n2 is None:
-        assert d["col2_spec"] == -1
+        assert d["col2_spec"] == -1 and d["col3_spec"] == -1
     else:
         assert d["col2_spec"] >= 0 and (d["col2_n1"], d["col2_n2"]) == n1n2
         assert d["col2_n1"] * d["col2_n2"] == h
+        assert d["col3_spec"] == -1  # the three-stage kernel is opt-in (ILS_COL3_SPEC)
     if (h, w) == (1080, 1920):
         assert d["row_radix"] == [32, 30] and d["row_swz"] == 3 and d["row_band"] == 6
         assert 3 * (d["row_smem"] + 1024) <= 228 * 1024

@@ -34,11 +34,52 @@ def _penalties():
     ]
 
 
-def test_plan_uses_the_two_stage_4320_column_kernel():
+def test_plan_uses_the_staged_4320_column_kernels():
     from paper_2003_07504_b200 import _lib, _runtime as rt
 
     p = rt.get_plan(1, 4320, 256, ils.SmoothParams(ils.Welsch(0.1), 1.0).c_params(), _lib.ILS_F32, 0)
-    assert (p.info["col2_n1"], p.info["col2_n2"]) == (72, 60)
+    assert (p.info["col2_n1"], p.info["col2_n2"]) == (72, 60) and p.info["col3_spec"] == -1
+
+
+@pytest.mark.parametrize("H", [1080, 2160, 4320])
+def test_three_stage_and_two_stage_column_solves_agree(H, monkeypatch):
+    # k_col3 (opt-in, ILS_COL3_SPEC=-2) and k_col2 (default) on the same plane: both
+    # within the north-star tolerance of the oracle, and within fp32 noise of each other
+    import ctypes as C
+
+    from paper_2003_07504_b200 import _lib
+
+    params = ils.SmoothParams(ils.Welsch(C5["gamma"]), C5["lam"], iters=C5["iters"], c=C5["c"])
+    f = np.random.default_rng(H).random((H, 64))
+    ft = torch.from_numpy(f).to("cuda", torch.float32)[None]
+    L = _lib.lib()
+    outs = []
+    for env in ("-2", None):  # the opt-in three-stage kernel, then the default k_col2
+        if env is None:
+            monkeypatch.delenv("ILS_COL3_SPEC", raising=False)
+        else:
+            monkeypatch.setenv("ILS_COL3_SPEC", env)
+        h = C.c_void_p()
+        _lib.check(L.ils_plan_create(C.byref(h), 1, H, 64, C.byref(ils.penalty.params_of(params)), _lib.ILS_F32, 0))
+        info = _lib.PlanInfo()
+        L.ils_plan_get_info(h, C.byref(info))
+        assert (info.col3_spec >= 0) == (env is not None)
+        ws_sz = C.c_size_t()
+        L.ils_workspace_size(h, C.byref(ws_sz))
+        ws = torch.empty(ws_sz.value, dtype=torch.uint8, device="cuda")
+        st = torch.empty(1, dtype=torch.int32, device="cuda")
+        u = torch.empty_like(ft)
+        _lib.check(L.ils_smooth(h, C.c_void_p(ft.data_ptr()), C.c_void_p(u.data_ptr()), H * 64,
+                                C.c_void_p(ws.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                C.c_void_p(st.data_ptr()), None))
+        torch.cuda.synchronize()
+        assert int(st.item()) == _lib.STATUS_CLEAN
+        outs.append(u[0].double().cpu().numpy())
+        L.ils_plan_destroy(h)
+    ref = O.smooth_plane(f, O.Welsch(C5["gamma"]), C5["lam"], C5["iters"], c=C5["c"], workers=WORKERS)
+    for u in outs:
+        assert np.max(np.abs(u - ref)) <= 1e-4
+    assert np.max(np.abs(outs[0] - outs[1])) <= 2e-5
 
 
 @pytest.mark.parametrize("W", [64, 256])

@@ -92,7 +92,7 @@ def test_plan_denom_and_f_hat_follow_the_reference_contract(g):
         h, w = f.shape
         plan = ils.make_plan(h, w, 1.5, 4.0, f)
         assert plan.denom.shape == (h, w) and plan.denom.dtype == np.float64
-        assert np.allclose(plan.denom, g[name + "_denom"], rtol=1e-15, atol=0)
+        assert np.allclose(plan.denom, g[name + "_denom"], rtol=1e-13, atol=0)  # GPU vs libm cos ulps
         assert plan.f_hat.dtype == np.complex128
         assert np.max(np.abs(plan.f_hat - g[name + "_fhat"])) <= 1e-12 * max(1.0, np.max(np.abs(g[name + "_fhat"])))
         # hqs.py:61 rebinds f_hat with dataclasses.replace

@@ -1,0 +1,32 @@
+"""Per-SASS-region stall attribution from an ncu source-page CSV (--print-source sass).
+
+    ncu -i rep.ncu-rep --page source --csv --print-source sass --kernel-name regex:k_row > x.csv
+    python tools/ncu_sass_hot.py x.csv [--reason stall_long_sb] [--top 30] [--context 3]
+"""
+import argparse
+import csv
+
+ap = argparse.ArgumentParser()
+ap.add_argument("csv")
+ap.add_argument("--reason", default="Warp Stall Sampling (All Samples)")
+ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--context", type=int, default=0)
+a = ap.parse_args()
+rows = list(csv.reader(open(a.csv)))
+hdr = rows[1]
+data = [dict(zip(hdr, r)) for r in rows[2:]]
+num = lambda d, k: float(d.get(k) or 0)  # noqa: E731
+tot = sum(num(d, a.reason) for d in data)
+reasons = [k for k in hdr if k.startswith("stall_") and "Not Issued" not in k]
+print(f"{a.reason}: {tot:.0f} samples, {sum(num(d, 'Instructions Executed') for d in data):.0f} warp instructions")
+print({r: int(sum(num(d, r) for d in data)) for r in reasons if sum(num(d, r) for d in data) > 0})
+top = sorted(range(len(data)), key=lambda i: -num(data[i], a.reason))[: a.top]
+shown = set()
+for i in sorted(top):
+    for j in range(max(0, i - a.context), min(len(data), i + 1)):
+        if j in shown:
+            continue
+        shown.add(j)
+        d = data[j]
+        why = ",".join(f"{r[6:]}={int(num(d, r))}" for r in reasons if num(d, r) > 0)
+        print(f"{j:5d} {d['Source'][:64]:64s} {num(d, a.reason):5.0f} x{int(num(d, 'Instructions Executed')):6d} {why}")
