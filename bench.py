@@ -68,7 +68,7 @@ WORKLOAD = "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters"
 def config_of(world):
     """The `config` both arms print (identical dicts)."""
     return {"workload": WORKLOAD, "parallelism": f"frame-sharded x{world}",
-            "l2": "inputs larger than L2 (16 frames x 24.9 MB per step per GPU)"}
+            "l2": "inputs larger than L2 (32 frames x 24.9 MB per step per GPU)"}
 
 
 def cpu_model():
@@ -402,7 +402,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--frames", type=int, default=16, help="frames per step per GPU")
+    ap.add_argument("--frames", type=int, default=32, help="frames per step per GPU")
     ap.add_argument("--group", type=int, default=1, help="frames per ils_smooth call (L2-resident group)")
     ap.add_argument("--streams", type=int, default=2, help="concurrent frame-group lanes (graph branches)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
