@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   mbar_fence_init();
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
   pdl_trigger();
-  if (IT)  // the first steps' f rows into L2 (f is the call's input: no wait needed)
-    for (int y = r0 + tid; y < min(r1, r0 + 3 * NG); y += kRowThreads)
+  if (IT)  // the chunk's f rows into L2 (f is the call's input: no wait needed)
+    for (int y = r0 + tid; y < r1; y += kRowThreads)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fpl + (size_t)y * A.f_rp),
                    "r"((unsigned)(W * sizeof(T)))
                    : "memory");
@@ -152,20 +152,6 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
 
   for (int j = r0; j < r1; j += NG) {
     const int ng = min(NG, r1 - j);
-    // the rows two steps ahead into L2 (their TMA loads are issued at the end
-    // of the next step and waited for right after: they should hit L2)
-    if (tid < NG && j + (2 + PF) * NG + 1 + tid <= r1) {
-      const int y = wrapi(j + (2 + PF) * NG + 1 + tid, H);
-      const void* src = IT ? static_cast<const void*>(Sin_b + (size_t)y * S_rp) : static_cast<const void*>(fpl + (size_t)y * f_rp);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(IT ? spec_bytes : (unsigned)(W * sizeof(T)))
-                   : "memory");
-    } else if (IT && tid >= 32 && tid < 32 + NG && j + 3 * NG + tid - 32 < r1) {
-      // and the f rows the r2c adds three steps from now (at 3840 / 7680 wide
-      // the frame's f does not stay in L2 next to its spectra)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fpl + (size_t)(j + 3 * NG + tid - 32) * f_rp),
-                   "r"((unsigned)(W * sizeof(T)))
-                   : "memory");
-    }
     // ---- A: u rows j+1 .. j+ng
     for (int i = g.id; i < ng; i += NG) ILS_ROLL_LAND((p + 1 + i) % NS);
     for (int i = 0; i < ng; ++i) phase ^= 1u << ((p + 1 + i) % NS);

@@ -2,7 +2,8 @@
 DRAM bytes, L2 hit rate, issue utilisation, SM-active vs elapsed cycles and
 the top warp-stall reasons; and refresh profiles/traffic.json.
 
-    python tools/ncu_summary.py gpurun_out/seq_full.ncu-rep profiles/r01_seq_full_summary.txt
+    python tools/ncu_summary.py gpurun_out/seq_full.ncu-rep profiles/r02_seq_full_summary.txt
+    python tools/ncu_summary.py gpurun_out/seq_4k.ncu-rep profiles/r02_seq_4k_summary.txt "one 4K RGB frame" traffic_4k.json
 """
 import csv
 import io
@@ -40,7 +41,7 @@ def short(name):
     return base.replace("void ", "")
 
 
-def main(rep, out_txt):
+def main(rep, out_txt, what="one 1080p RGB frame", traffic_name="traffic.json"):
     h, units, rows = raw(rep)
     lines, kern = [], []
     for r in rows:
@@ -77,7 +78,7 @@ def main(rep, out_txt):
             f"warps/SM {d.get('warps_active_per_sm', 0):5.2f}  SM-active/elapsed {sa:4.2f}  regs {d.get('registers', 0):.0f}")
         lines.append("    stalls (cycles per issued instruction): "
                      + ", ".join(f"{k} {v}" for k, v in d["top_stalls_cycles_per_issue"].items()))
-    hdr = (f"# ncu --set full summary of {os.path.basename(rep)} (one 1080p RGB frame's pass sequence, "
+    hdr = (f"# ncu --set full summary of {os.path.basename(rep)} ({what}'s pass sequence, "
            "--cache-control none: warm L2 as in the real sequence, --clock-control none)\n")
     with open(out_txt, "w") as fh:
         fh.write(hdr + "\n".join(lines) + "\n")
@@ -86,6 +87,10 @@ def main(rep, out_txt):
     agg = {}
     for d in kern:
         k = d["kernel"]
+        if "k_row_roll" in k:
+            tag = "k_row_roll_it" if ", 1, " in k else "k_row_roll_f0"
+            agg.setdefault(tag, []).append(d)
+            continue
         tag = ("k_row_it" if ", 1>" in k or k.endswith("1>") else
                "k_row_f0" if k.endswith("0>") else "k_row_fin" if k.endswith("3>") else
                "k_col2" if "k_col2" in k else "k_col" if "k_col" in k else None)
@@ -101,9 +106,9 @@ def main(rep, out_txt):
                    "duration_us": sum(x.get("duration", 0) for x in ds) / n,
                    "issue_active_pct": sum(x.get("issue_active_pct", 0) for x in ds) / n,
                    "launches": n, "source": out_txt}
-    with open(os.path.join(os.path.dirname(out_txt), "traffic.json"), "w") as fh:
+    with open(os.path.join(os.path.dirname(out_txt), traffic_name), "w") as fh:
         json.dump(tj, fh, indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:])
