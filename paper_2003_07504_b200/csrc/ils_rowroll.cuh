@@ -81,11 +81,14 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   mbar_fence_init();
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
   pdl_trigger();
-  if (IT)  // the chunk's f rows into L2 (f is the call's input: no wait needed)
+#ifdef ILS_ROLL_F_PREFETCH  // (tuning: the chunk's f rows into L2 up front -- at 3840 wide the
+                            // frame does not fit L2 and the rows are read twice: +100 MB DRAM)
+  if (IT)
     for (int y = r0 + tid; y < r1; y += kRowThreads)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fpl + (size_t)y * A.f_rp),
                    "r"((unsigned)(W * sizeof(T)))
                    : "memory");
+#endif
   __syncthreads();  // barriers initialised, twiddle table staged
   pdl_wait();
 
