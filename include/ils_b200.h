@@ -270,6 +270,28 @@ ILS_API ils_status ils_slab_row_pass(const ils_plan* plan, int32_t mode, const v
 /* Column solve pass on this rank's columns: fwd recv -> rev send. */
 ILS_API ils_status ils_slab_col_pass(const ils_plan* plan, void* fwd_recv, void* rev_send, void* stream);
 
+/* The whole C5 slab smooth in one call (SURVEY 8b's ils_smooth_dist): the row
+ * and column slab passes above with the two transposes per iteration as NCCL
+ * grouped send/recv (byte blocks in ils_slab_get_layout's order) on `stream`,
+ * for `planes` consecutive planes of this rank (f_ext: [rows + 2][width]
+ * per plane, f_ext_stride elements apart; u: [rows][width], u_stride apart).
+ * nccl_comm is an ncclComm_t over the slab plan's nranks, rank = its rank
+ * (ils_nccl_comm_create, or the caller's own).  NCCL is loaded at run time
+ * (libnccl.so.2, or the path in ILS_NCCL_LIB).  workspace:
+ * ils_dist_workspace_size bytes (the four all-to-all buffers).  Asynchronous;
+ * bitwise the single-GPU ils_smooth result on this rank's rows. */
+typedef struct {
+  char internal[128]; /* ncclUniqueId */
+} ils_nccl_id;
+ILS_API ils_status ils_nccl_get_unique_id(ils_nccl_id* id);
+ILS_API ils_status ils_nccl_comm_create(void** comm, int32_t nranks, const ils_nccl_id* id, int32_t rank,
+                                        int32_t device);
+ILS_API ils_status ils_nccl_comm_destroy(void* comm);
+ILS_API ils_status ils_dist_workspace_size(const ils_plan* slab_plan, size_t* bytes);
+ILS_API ils_status ils_smooth_dist(const ils_plan* slab_plan, const void* f_ext_dev, void* u_dev, int32_t planes,
+                                   int64_t f_ext_stride, int64_t u_stride, void* workspace, void* nccl_comm,
+                                   void* stream, int32_t* status_dev);
+
 /* Introspection for tests and the bench. */
 typedef struct {
   int32_t batch, height, width, dtype, packed;

@@ -30,7 +30,8 @@ EXPORTS = (
     "ils_solve_ls", "ils_rfft2", "ils_irfft2", "ils_rgb_yuv", "ils_plan_get_info", "ils_last_error",
     "ils_abi_version", "ils_grad", "ils_adjoint_accumulate", "ils_aux_update", "ils_energy",
     "ils_convert", "ils_denominator", "ils_hermitian_full", "ils_tonemap_workspace_size", "ils_tonemap",
-    "ils_detail_boost",
+    "ils_detail_boost", "ils_nccl_get_unique_id", "ils_nccl_comm_create", "ils_nccl_comm_destroy",
+    "ils_dist_workspace_size", "ils_smooth_dist",
 )
 
 
@@ -46,6 +47,10 @@ class HqsParams(C.Structure):
 class TonemapParamsC(C.Structure):
     _fields_ = [("nscales", C.c_int32), ("lam", C.c_double * 3), ("weights", C.c_double * 3),
                 ("target_range", C.c_double), ("saturation", C.c_double), ("log_offset", C.c_double)]
+
+
+class NcclId(C.Structure):
+    _fields_ = [("internal", C.c_char * 128)]
 
 
 class Epilogue(C.Structure):
@@ -116,6 +121,11 @@ _SIGS = {
     "ils_tonemap_workspace_size": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
     "ils_tonemap": (C.c_int, [_P, _P, _P, _P, C.POINTER(TonemapParamsC), _P, _P, _P, _P]),
     "ils_detail_boost": (C.c_int, [_P, _P, _P, C.c_int64, C.c_double, C.c_int32, _P]),
+    "ils_nccl_get_unique_id": (C.c_int, [C.POINTER(NcclId)]),
+    "ils_nccl_comm_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.POINTER(NcclId), C.c_int32, C.c_int32]),
+    "ils_nccl_comm_destroy": (C.c_int, [_P]),
+    "ils_dist_workspace_size": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
+    "ils_smooth_dist": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, C.c_int64, _P, _P, _P, _P]),
     "ils_last_error": (C.c_char_p, []),
     "ils_abi_version": (C.c_int32, []),
 }

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <limits>
 #include <string>
 #include <vector>
@@ -1978,6 +1979,174 @@ ils_status ils_slab_col_pass(const ils_plan* p, void* recv, void* send, void* st
   if (p->dtype == ILS_F32)
     return slab_col_t<float>(p, static_cast<cx<float>*>(recv), static_cast<cx<float>*>(send), s);
   return slab_col_t<double>(p, static_cast<cx<double>*>(recv), static_cast<cx<double>*>(send), s);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ C5 over NCCL in one call
+// The slab smooth of dist.SlabSmoother as a C entry point: the row / column
+// slab passes above with the two transposes as NCCL grouped send/recv on the
+// caller's stream.  NCCL is bound at run time (dlopen of libnccl.so.2, or
+// ILS_NCCL_LIB), so the library has no link-time NCCL dependency and a
+// process that never calls these functions never loads it.
+#include <dlfcn.h>
+
+namespace {
+
+struct NcclApi {
+  bool loaded = false;
+  std::string error;
+  int (*get_unique_id)(ils_nccl_id*) = nullptr;
+  int (*comm_init_rank)(void**, int, ils_nccl_id, int) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
+  const char* (*error_string)(int) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* path = getenv("ILS_NCCL_LIB");
+    void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      api.error = std::string("cannot load NCCL: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.get_unique_id = reinterpret_cast<int (*)(ils_nccl_id*)>(sym("ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<int (*)(void**, int, ils_nccl_id, int)>(sym("ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<int (*)(void*)>(sym("ncclCommDestroy"));
+    api.send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(sym("ncclSend"));
+    api.recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(sym("ncclRecv"));
+    api.group_start = reinterpret_cast<int (*)()>(sym("ncclGroupStart"));
+    api.group_end = reinterpret_cast<int (*)()>(sym("ncclGroupEnd"));
+    api.error_string = reinterpret_cast<const char* (*)(int)>(sym("ncclGetErrorString"));
+    api.loaded = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.send && api.recv &&
+                 api.group_start && api.group_end;
+    if (!api.loaded) api.error = "NCCL library lacks the point-to-point API";
+  });
+  return api;
+}
+
+constexpr int kNcclUint8 = 1;  // ncclUint8: blocks move as bytes
+
+ils_status nccl_fail(const char* what, int r) {
+  const NcclApi& n = nccl();
+  return fail(ILS_ECUDA, "%s: NCCL error %d (%s)", what, r, n.error_string ? n.error_string(r) : "?");
+}
+
+// block sizes in bytes per peer for the four all-to-all buffers (ils_slab_get_layout)
+struct DistLayout {
+  size_t bytes[4][kMaxSeg];
+  size_t off[4][kMaxSeg];
+  size_t total[4];
+};
+
+DistLayout dist_layout(const ils_plan* p) {
+  DistLayout d{};
+  int64_t counts[4 * kMaxSeg];
+  ils_slab_get_layout(p, nullptr, nullptr, nullptr, counts);
+  const size_t elt = p->dtype == ILS_F32 ? sizeof(cx<float>) : sizeof(cx<double>);
+  for (int k = 0; k < 4; ++k) {
+    size_t o = 0;
+    for (int q = 0; q < p->P; ++q) {
+      d.bytes[k][q] = (size_t)counts[k * kMaxSeg + q] * elt;
+      d.off[k][q] = o;
+      o += d.bytes[k][q];
+    }
+    d.total[k] = (o + 255) & ~size_t(255);
+  }
+  return d;
+}
+
+ils_status dist_a2a(const ils_plan* p, const DistLayout& d, int sk, int rk, const char* send, char* recv, void* comm,
+                    cudaStream_t s) {
+  const NcclApi& n = nccl();
+  int r = n.group_start();
+  if (r) return nccl_fail("ncclGroupStart", r);
+  for (int q = 0; q < p->P; ++q) {
+    if (d.bytes[sk][q] && (r = n.send(send + d.off[sk][q], d.bytes[sk][q], kNcclUint8, q, comm, s))) break;
+    if (d.bytes[rk][q] && (r = n.recv(recv + d.off[rk][q], d.bytes[rk][q], kNcclUint8, q, comm, s))) break;
+  }
+  const int r2 = n.group_end();
+  if (r) return nccl_fail("ncclSend/ncclRecv", r);
+  if (r2) return nccl_fail("ncclGroupEnd", r2);
+  return ILS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ils_status ils_nccl_get_unique_id(ils_nccl_id* id) {
+  if (!id) return fail(ILS_EINVAL, "NULL argument");
+  const NcclApi& n = nccl();
+  if (!n.loaded) return fail(ILS_ECUDA, "%s", n.error.c_str());
+  const int r = n.get_unique_id(id);
+  return r ? nccl_fail("ncclGetUniqueId", r) : ILS_OK;
+}
+
+ils_status ils_nccl_comm_create(void** comm, int32_t nranks, const ils_nccl_id* id, int32_t rank, int32_t device) {
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(ILS_EINVAL, "bad communicator arguments");
+  const NcclApi& n = nccl();
+  if (!n.loaded) return fail(ILS_ECUDA, "%s", n.error.c_str());
+  DeviceGuard dg(device);
+  const int r = n.comm_init_rank(comm, nranks, *id, rank);
+  return r ? nccl_fail("ncclCommInitRank", r) : ILS_OK;
+}
+
+ils_status ils_nccl_comm_destroy(void* comm) {
+  if (!comm) return ILS_OK;
+  const NcclApi& n = nccl();
+  if (!n.loaded) return fail(ILS_ECUDA, "%s", n.error.c_str());
+  const int r = n.comm_destroy(comm);
+  return r ? nccl_fail("ncclCommDestroy", r) : ILS_OK;
+}
+
+ils_status ils_dist_workspace_size(const ils_plan* p, size_t* bytes) {
+  if (!p || !p->slab || !bytes) return fail(ILS_EINVAL, "not a slab plan");
+  const DistLayout d = dist_layout(p);
+  *bytes = d.total[0] + d.total[1] + d.total[2] + d.total[3];
+  return ILS_OK;
+}
+
+ils_status ils_smooth_dist(const ils_plan* p, const void* f_ext, void* u, int32_t planes, int64_t f_ext_stride,
+                           int64_t u_stride, void* ws, void* comm, void* stream, int32_t* status) {
+  if (!p || !p->slab) return fail(ILS_EINVAL, "not a slab plan");
+  if (!p->d_tables) return fail(ILS_EINVAL, "plan was created host-only (device < 0)");
+  if (!f_ext || !u || !ws || !comm || !status || planes < 1) return fail(ILS_EINVAL, "NULL argument");
+  if (f_ext_stride < (int64_t)(p->Hl + 2) * p->W || u_stride < (int64_t)p->Hl * p->W)
+    return fail(ILS_EINVAL, "plane strides smaller than the rank's rows");
+  const NcclApi& n = nccl();
+  if (!n.loaded) return fail(ILS_ECUDA, "%s", n.error.c_str());
+  DeviceGuard dg(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const DistLayout d = dist_layout(p);
+  char* fwd_send = static_cast<char*>(ws);
+  char* fwd_recv = fwd_send + d.total[0];
+  char* rev_send = fwd_recv + d.total[1];
+  char* rev_recv = rev_send + d.total[2];
+  ILS_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t), s));
+  const int iters = p->prm.iters;
+  const size_t es = p->dtype == ILS_F32 ? 4 : 8;
+  for (int c = 0; c < planes; ++c) {  // dist.SlabSmoother.smooth, one plane after the other
+    const char* fe = static_cast<const char*>(f_ext) + (size_t)c * f_ext_stride * es;
+    char* uc = static_cast<char*>(u) + (size_t)c * u_stride * es;
+    ils_status st = ils_slab_row_pass(p, MODE_F0, fe, nullptr, fwd_send, nullptr, 0, stream, status);
+    for (int it = 0; it < iters && st == ILS_OK; ++it) {
+      st = dist_a2a(p, d, 0, 1, fwd_send, fwd_recv, comm, s);
+      if (st == ILS_OK) st = ils_slab_col_pass(p, fwd_recv, rev_send, stream);
+      if (st == ILS_OK) st = dist_a2a(p, d, 2, 3, rev_send, rev_recv, comm, s);
+      if (st == ILS_OK && it + 1 < iters) st = ils_slab_row_pass(p, MODE_IT, fe, rev_recv, fwd_send, nullptr, it + 1, stream, status);
+    }
+    if (st == ILS_OK) st = ils_slab_row_pass(p, MODE_FIN, fe, rev_recv, nullptr, uc, iters, stream, status);
+    if (st != ILS_OK) return st;
+  }
+  return ILS_OK;
 }
 
 }  // extern "C"

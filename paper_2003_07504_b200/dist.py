@@ -290,3 +290,54 @@ class EmulatedSlab:
                 _lib.lib().ils_plan_destroy(h)
         except Exception:
             pass
+
+
+class NcclSlab:
+    """C5 through the library's own C entry point (ils_smooth_dist): the slab
+    passes with the transposes as NCCL send/recv issued from C, on one
+    NCCL communicator the library creates (ils_nccl_comm_create) -- the
+    unique id travels over the caller's torch.distributed group (any
+    backend), or nothing when nranks == 1.
+    """
+
+    def __init__(self, height, width, params, nranks, rank, device=0, group=None, dtype_code=_lib.ILS_F32):
+        import torch
+
+        self.torch = torch
+        self.plan, self.lay = slab_layout(height, width, params_of(params), dtype_code, nranks, rank, device=device)
+        L = _lib.lib()
+        nid = _lib.NcclId()
+        if rank == 0:
+            _lib.check(L.ils_nccl_get_unique_id(C.byref(nid)), "ils_nccl_get_unique_id")
+        if nranks > 1:
+            import torch.distributed as dist
+
+            box = [bytes(nid.internal) if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0, group=group)
+            C.memmove(C.addressof(nid), box[0], 128)
+        self.comm = C.c_void_p()
+        _lib.check(L.ils_nccl_comm_create(C.byref(self.comm), nranks, C.byref(nid), rank, device),
+                   "ils_nccl_comm_create")
+        ws = C.c_size_t()
+        _lib.check(L.ils_dist_workspace_size(self.plan, C.byref(ws)), "ils_dist_workspace_size")
+        self.ws = torch.empty(ws.value, dtype=torch.uint8, device=torch.device("cuda", device))
+        self.status = torch.empty(1, dtype=torch.int32, device=torch.device("cuda", device))
+        self.W = width
+
+    def smooth(self, f_ext, u):
+        """f_ext: [planes, rows + 2, W] (halo rows included), u: [planes, rows, W], CUDA, contiguous."""
+        torch = self.torch
+        P = f_ext.shape[0]
+        _lib.check(_lib.lib().ils_smooth_dist(self.plan, C.c_void_p(f_ext.data_ptr()), C.c_void_p(u.data_ptr()), P,
+                                              f_ext[0].numel(), u[0].numel(), C.c_void_p(self.ws.data_ptr()),
+                                              self.comm, C.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                              C.c_void_p(self.status.data_ptr())), "ils_smooth_dist")
+        return u
+
+    def close(self):
+        if getattr(self, "comm", None):
+            _lib.lib().ils_nccl_comm_destroy(self.comm)
+            self.comm = None
+        if getattr(self, "plan", None):
+            _lib.lib().ils_plan_destroy(self.plan)
+            self.plan = None

@@ -94,3 +94,50 @@ def test_slab_processes_bitwise_equal_single_gpu(world, H, W, kind):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
+
+
+@pytest.mark.parametrize("H,W,planes", [(360, 640, 3), (1080, 1920, 1), (4320, 7680, 1)])
+def test_smooth_dist_c_entry_nccl_one_rank_bitwise(H, W, planes):
+    # ils_smooth_dist (C ABI: slab passes + NCCL send/recv issued from C) on a
+    # 1-rank communicator the library creates: bitwise the 1-GPU ils_smooth
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib
+    from paper_2003_07504_b200 import dist as D
+
+    params = ils.SmoothParams(ils.Welsch(10 / 255), 30.0, iters=3, c=2.0)
+    img = torch.from_numpy(np.random.default_rng(H).random((planes, H, W))).to("cuda", torch.float32)
+    ns = D.NcclSlab(H, W, params, 1, 0, device=0)
+    try:
+        rows = D.halo_rows(H, 0, H)
+        f_ext = img[:, rows].contiguous()
+        u = torch.empty((planes, H, W), device="cuda")
+        ns.smooth(f_ext, u)
+        torch.cuda.synchronize()
+        assert int(ns.status.item()) == _lib.STATUS_CLEAN
+        ref = ils.smooth_batch(img, params)
+        assert torch.equal(u, ref)
+    finally:
+        ns.close()
+
+
+def test_smooth_dist_rejects_non_slab_plans_and_bad_strides():
+    import ctypes as C
+
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+    from paper_2003_07504_b200 import dist as D
+
+    params = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1.0)
+    plan = rt.get_plan(1, 64, 64, params.c_params(), _lib.ILS_F32, 0)
+    L = _lib.lib()
+    buf = torch.empty(1 << 16, device="cuda")
+    rc = L.ils_smooth_dist(plan.ptr, C.c_void_p(buf.data_ptr()), C.c_void_p(buf.data_ptr()), 1, 66 * 64, 64 * 64,
+                           C.c_void_p(buf.data_ptr()), C.c_void_p(1), None, C.c_void_p(buf.data_ptr()))
+    assert rc == _lib.ILS_EINVAL and "slab" in _lib.last_error()
+    ns = D.NcclSlab(64, 64, params, 1, 0, device=0)
+    try:
+        rc = L.ils_smooth_dist(ns.plan, C.c_void_p(buf.data_ptr()), C.c_void_p(buf.data_ptr()), 1, 64 * 64, 64 * 64,
+                               C.c_void_p(ns.ws.data_ptr()), ns.comm, None, C.c_void_p(ns.status.data_ptr()))
+        assert rc == _lib.ILS_EINVAL  # f_ext must hold the rows plus two halo rows
+    finally:
+        ns.close()
