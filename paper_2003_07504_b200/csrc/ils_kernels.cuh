@@ -390,10 +390,15 @@ constexpr int kTwSplitMax = 32;  // entries of the w^(32 m) table (N/2 < 32 * 32
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
 // O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
 // (complex operations: the packed FP32x2 forms in fp32 translation units)
+// (N and the group size are compile-time constants for the compile-time row
+// plans: the loop then unrolls, with the k == 0 / k == N/2 cases folded)
 template <typename T, class TW, class Grp>
 __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const TW& tw, const Grp& g) {
-  int m = 0;
-  for (int k = g.rank; k <= N / 2; k += g.size(), ++m) {
+  const int M = (N / 2) / g.size() + 1;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int k = g.rank + m * g.size();
+    if (k > N / 2) break;
     if (k == 0) {
       const cx<T> z0 = z[0];
       z[0] = cx<T>{z0.x + z0.y, T(0)};
@@ -416,8 +421,11 @@ __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const TW& tw, const Gr
 // N-point FFT of Z then yields W * (x[2n] + i x[2n+1]) of the c2r of X/W.
 template <typename T, class TW, class Grp>
 __device__ __forceinline__ void c2r_pre(cx<T>* z, int N, const TW& tw, const Grp& g) {
-  int m = 0;
-  for (int k = g.rank; k <= N / 2; k += g.size(), ++m) {
+  const int M = (N / 2) / g.size() + 1;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int k = g.rank + m * g.size();
+    if (k > N / 2) break;
     if (k == 0) {
       const T a = z[0].x, c = z[N].x;  // DC / Nyquist: imaginary parts ignored (as irfft)
       z[0] = cx<T>{a + c, a - c};
@@ -572,6 +580,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     if (tid * 32 <= A.N / 2) s_whi[tid] = A.wreal[32 * tid];
     __syncthreads();
   }
+  const int NPK = (FS::n > 0 && PACKED) ? FS::n : A.N;  // packed line length (compile-time for specs)
   using TwT = std::conditional_t<WSPLIT, TwSplit<T>, TwTab<T, WSMEM>>;
   TwT twp;
   if constexpr (WSPLIT) twp = TwSplit<T>{ldg_cx(A.wreal + (tid % 32)), s_whi};
@@ -736,7 +745,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
           for (int x = g.rank; x < W; x += g.size()) L.set(i, x, fpl[(size_t)y * A.f_rp + x]);
       } else {
         if (PACKED) {
-          c2r_pre<T>(z, A.N, twp, g);
+          c2r_pre<T>(z, NPK, twp, g);
         } else {
           // Hermitian completion X[W-k] = conj X[k]; DC imaginary part dropped
           for (int k = A.Wc + g.rank; k < W; k += g.size()) z[k] = conj(z[W - k]);
@@ -1057,7 +1066,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
       }
       fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
     }
-    if (PACKED) r2c_post<T>(z, A.N, twp, g);
+    if (PACKED) r2c_post<T>(z, NPK, twp, g);
     else g.sync();
     if (A.sout_seg.n == 0) {
       cx<T>* dst = A.Sout + (size_t)b * A.S_ps + (size_t)(r0 + i) * A.S_rp;

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   do {                                                                                                           \
     mbar_wait(&bars[slot], (phase >> (slot)) & 1u);                                                              \
     if (IT) {                                                                                                    \
-      c2r_pre<T>(L.line(slot), A.N, TwTab<T, WSMEM>{swreal}, g);                                                  \
+      c2r_pre<T>(L.line(slot), FS::n, TwTab<T, WSMEM>{swreal}, g);                                                \
       fft_line<T, +1, FS>(L.line(slot), A.fft, g, NoPre{}, &twc);                                                \
     }                                                                                                            \
   } while (0)
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
       } else {
         fft_line<T, -1, FS>(z, A.fft, g, NoPre{}, &twc);
       }
-      r2c_post<T>(z, A.N, TwTab<T, WSMEM>{swreal}, g);
+      r2c_post<T>(z, FS::n, TwTab<T, WSMEM>{swreal}, g);
       if (g.rank == 0) {
         bulk_s2g(A.Sout + (size_t)b * A.S_ps + (size_t)(j + i) * A.S_rp, z, spec_bytes);
         if (i < ngn) {  // full steps: slot (p + i) hosts row jn + 1 + i

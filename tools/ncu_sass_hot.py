@@ -11,10 +11,16 @@ ap.add_argument("csv")
 ap.add_argument("--reason", default="Warp Stall Sampling (All Samples)")
 ap.add_argument("--top", type=int, default=25)
 ap.add_argument("--context", type=int, default=0)
+ap.add_argument("--kernel", type=int, default=0, help="which kernel section of the CSV")
 a = ap.parse_args()
 rows = list(csv.reader(open(a.csv)))
-hdr = rows[1]
-data = [dict(zip(hdr, r)) for r in rows[2:]]
+# the CSV may hold several kernels, each a "Kernel Name" row then a header row
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+k = min(a.kernel, len(starts) - 1)
+end = starts[k + 1] if k + 1 < len(starts) else len(rows)
+print(rows[starts[k]][1][:140])
+hdr = rows[starts[k] + 1]
+data = [dict(zip(hdr, r)) for r in rows[starts[k] + 2:end]]
 num = lambda d, k: float(d.get(k) or 0)  # noqa: E731
 tot = sum(num(d, a.reason) for d in data)
 reasons = [k for k in hdr if k.startswith("stall_") and "Not Issued" not in k]
