@@ -107,3 +107,30 @@ def test_blur_and_tonemap_behaviour():
         ils.tonemap_single(np.zeros((8, 8)), ils.MultiImage((lum[:8, :8],) * 3, ils.RGB), tp)
     with pytest.raises(ValueError):
         ils.texture_smooth(ils.MultiImage.from_array(np.full((8, 8, 3), 0.5)), 10 / 255, 30.0, sigma_pre=-1.0)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_tonemap_batched_lambdas_equal_separate_plans(prec):
+    # ils_tonemap smooths the three scales as ONE batched launch sequence with a
+    # per-plane lambda table; each base must be the smooth of a plan built for
+    # its own lambda (applications.py:165-168): rebuild the reference formula
+    # (:170-183) on top of three separate smooth_batch calls and compare
+    import torch
+
+    rng = np.random.default_rng(12)
+    lum = 10.0 ** rng.uniform(-2, 2, (40, 56))
+    rgb_planes = tuple(lum * t for t in (0.9, 0.7, 0.5))
+    rgb = ils.MultiImage(rgb_planes, ils.RGB)
+    base = ils.SmoothParams(ils.Charbonnier(1.0, 1e-4), 5.0)
+    tp = ils.TonemapParams(base, lambdas=(0.25, 2.0, 16.0), weights=(1.3, 0.7, 1.1), target_range=1.8)
+    got = ils.tonemap_multi(lum, rgb, tp, precision=prec).to_array()
+    dt = torch.float32 if prec == "fp32" else torch.float64
+    ll = np.log10(lum + tp.log_offset)
+    f = torch.from_numpy(ll).to("cuda", dt)[None]
+    b = [ils.smooth_batch(f, ils.SmoothParams(base.penalty, lam))[0].double().cpu().numpy() for lam in tp.lambdas]
+    spread = b[2].max() - b[2].min()
+    out = (b[2] - b[2].max()) * (tp.target_range / spread)
+    out = out + tp.weights[2] * (b[1] - b[2]) + tp.weights[1] * (b[0] - b[1]) + tp.weights[0] * (ll - b[0])
+    lum_out = 10.0 ** out
+    ref = np.stack([np.clip((c / lum) ** tp.saturation * lum_out, 0.0, 1.0) for c in rgb_planes], -1)
+    assert np.max(np.abs(got - ref)) < 1e-6  # (GPU vs numpy log10 ulps in the input; a lambda mix-up is ~1e-2)
