@@ -54,7 +54,7 @@ def test_rfft2_irfft2_match_numpy(shape, prec):
 
 
 # ------------------------------------------------------------ solve_ls
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 2e-4)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 2e-6)])  # fp32 measured 4.2e-7
 def test_solve_ls_matches_reference_goldens(g, prec, tol):
     worst = 0.0
     for key in g.files:
