@@ -30,6 +30,7 @@ e2e_dropin  the reference's own entry point, smooth_color(MultiImage of
           (pkg/src/ilsmooth/smoother.py:175-217), one image per call.
 parity    frame 0 of the device run against the float64 oracle
           (max-abs, PSNR: the north star's 1e-4 / 60 dB).
+c1, c2    BASELINE.json configs[0..1]: 512x512 and 1920x1080 gray frames/s.
 c4, c5    BASELINE.json configs[3..4]: 3840x2160 RGB video (256 frames,
           sharded over ranks, frames/s) and one 7680x4320 RGB image
           (Welsch, N=10; ms per image; at N > 1 the slab decomposition with
@@ -244,6 +245,65 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
+    """C1 / C2 (BASELINE.json configs[0..1]): gray frames of h x w, Charbonnier p=0.8, lambda=1,
+    N=4; device frames/s over 2 lanes, 32 frames per step (one plane each), CUDA graph, max over ranks."""
+    import torch
+
+    import paper_2003_07504_b200 as ils
+    from paper_2003_07504_b200 import _lib, _runtime as rt
+    from paper_2003_07504_b200.penalty import params_of
+
+    F = 32
+    prm = ils.SmoothParams(ils.Charbonnier(P_EXP, EPS), LAM, iters=ITERS)
+    plan = rt.get_plan(1, h, w, params_of(prm), _lib.ILS_F32, dev.index)
+    L = _lib.lib()
+    g = torch.Generator(device=dev)
+    g.manual_seed(20240607 + rank)
+    f = torch.rand((F, h, w), generator=g, device=dev)
+    u = torch.empty_like(f)
+    lanes = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev) for _ in lanes]
+    sts = [torch.empty(1, dtype=torch.int32, device=dev) for _ in lanes]
+
+    def launches(s):
+        lanes[1].wait_stream(s)
+        for k in range(F):
+            ln = k % 2
+            _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f[k].data_ptr()), C.c_void_p(u[k].data_ptr()), h * w,
+                                    C.c_void_p(wss[ln].data_ptr()), C.c_void_p((s if ln == 0 else lanes[1]).cuda_stream),
+                                    C.c_void_p(sts[ln].data_ptr()), None), "ils_smooth")
+        s.wait_stream(lanes[1])
+
+    with torch.cuda.stream(lanes[0]):
+        launches(lanes[0])
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=lanes[0]):
+        launches(lanes[0])
+    for _ in range(3):
+        graph.replay()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 20
+    with torch.cuda.stream(lanes[0]):
+        e0.record(lanes[0])
+        for _ in range(steps):
+            graph.replay()
+        e1.record(lanes[0])
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    for st in sts:
+        rt.raise_status(int(st.item()))
+    fps = world * F / (ms / 1e3)
+    peak, _ = peaks()
+    bpf = bytes_per_frame(ITERS, h, w, 1)
+    return {"workload": f"{label}: {w}x{h} gray ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
+            "value": round(fps, 1), "unit": "frames/s", "frames_per_step_per_gpu": F, "lanes": 2,
+            "whole_path": {"achieved": round(bpf * fps / world / 1e9, 1),
+                           "frac": round(bpf * fps / world / 1e9 / peak, 4), "bytes_per_frame": bpf}}
+
+
 def c4_leg(args, world, rank, dev, barrier, max_over_ranks):
     """C4: 3840x2160 RGB frames, Charbonnier N=4, args.c4_frames frames split over the ranks
     (no communication); aggregate frames/s over one pass of the whole batch, max over ranks.
@@ -413,6 +473,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cufft", action="store_true", help="skip the cuFFT + torch comparison leg")
+    ap.add_argument("--no-gray", action="store_true", help="skip the C1 / C2 (gray) legs")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (4K video) leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (8K image) leg")
     ap.add_argument("--no-dropin", action="store_true", help="skip the numpy drop-in (smooth_color) leg")
@@ -700,6 +761,12 @@ def main():
                          "(the reference's entry point, smoother.py:175-217), one image per call",
                   "output_dtype": str(out_img.channels[0].dtype)}
 
+    # ---- C1 / C2: gray frames (BASELINE.json configs[0..1])
+    c1 = c2 = None
+    if not args.no_gray:
+        c1 = gray_leg(args, world, rank, dev, barrier, max_over_ranks, 512, 512, "C1")
+        c2 = gray_leg(args, world, rank, dev, barrier, max_over_ranks, 1080, 1920, "C2")
+
     # ---- C4: 3840x2160 RGB video, 256 frames sharded over the ranks (BASELINE.json configs[3])
     c4 = None
     if not args.no_c4:
@@ -735,6 +802,8 @@ def main():
             "e2e_f32_planes": e2e_f32,
             "e2e_dropin": dropin,
             "parity": parity,
+            "c1": c1,
+            "c2": c2,
             "c4": c4,
             "c5": c5,
             "gpu_launches": launches,

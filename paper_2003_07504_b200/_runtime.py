@@ -298,18 +298,30 @@ def _parallel(fn, n):
 
 
 def to_device_planes(planes, precision=None):
-    """Host planes -> one CUDA tensor [B, H, W] of the target dtype (f64 over PCIe
-    through a pinned staging buffer, narrowed on the device)."""
+    """Host planes -> one CUDA tensor [B, H, W] of the target dtype.
+
+    Each plane is copied into its own pinned staging buffer and sent as soon
+    as that copy is done (one worker per plane, all host-to-device copies on
+    the caller's stream), so the PCIe transfer of plane i overlaps the host
+    copies of the others; fp32 targets are narrowed by the library's own
+    kernel (ils_convert)."""
     torch = _torch()
     dt = torch_dtype(precision)
     arrs = [np.asarray(p, dtype=np.float64) for p in planes]
     B = len(arrs)
     H, W = arrs[0].shape
-    stage = _pinned("in", (B, H, W), torch.float64)
-    host = stage.numpy()
-    _parallel(lambda i: np.copyto(host[i], arrs[i]), B)
-    dev = stage.to("cuda", non_blocking=True)
-    _pinned_done("in", torch.cuda.current_stream())
+    stream = torch.cuda.current_stream()
+    dev = torch.empty((B, H, W), dtype=torch.float64, device=stream.device)
+    stages = [_pinned(f"in{i}", (H, W), torch.float64) for i in range(B)]
+
+    def one(i):
+        np.copyto(stages[i].numpy(), arrs[i])
+        with torch.cuda.stream(stream):
+            dev[i].copy_(stages[i], non_blocking=True)
+
+    _parallel(one, B)
+    for i in range(B):
+        _pinned_done(f"in{i}", stream)
     if dt == torch.float64:
         return dev
     out = torch.empty((B, H, W), dtype=dt, device=dev.device)  # narrowed by the library's own kernel

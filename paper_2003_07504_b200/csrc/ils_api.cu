@@ -364,7 +364,10 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
 #ifdef ILS_ROW_MINB
     const int reg_cap = ILS_ROW_MINB;
 #else
-    const int reg_cap = p.row_spec >= 0 ? (p.N >= 3840 ? 1 : 3) : 2;  // kRowBlocksOf
+    // (the cost model's resident-CTA cap: kRowBlocksOf, except that the
+    // 1920-point plan keeps the 3-CTA model it was tuned with -- its band
+    // choice, 5, measured best; shared memory holds it to one CTA anyway)
+    const int reg_cap = p.row_spec >= 0 ? (p.N >= 3840 ? 1 : 3) : 2;
 #endif
     const int per_sm = (int)std::min<size_t>(reg_cap, (228 * 1024) / (smem + 1024));
     const long ctas = (long)p.B * ((p.H + band - 1) / band);

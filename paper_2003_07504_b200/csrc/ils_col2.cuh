@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
 // 30 x 36 by ~1% in the bench, and it does not spill)
 #define ILS_COL2_SPECS(X)                                                                                    \
   X(0, 36, 30, 8, 2) X(5, 30, 36, 8, 2) X(1, 36, 30, 6, 3) X(2, 36, 30, 4, 4) X(3, 36, 30, 10, 1) X(4, 36, 30, 10, 2) \
-      X(6, 36, 30, 16, 1) X(9, 45, 48, 8, 1) X(7, 48, 45, 4, 2) \
-      X(8, 48, 45, 8, 1) X(10, 72, 60, 4, 1)
+      X(6, 36, 30, 16, 1) X(8, 48, 45, 8, 1) X(9, 45, 48, 8, 1) X(7, 48, 45, 4, 2) \
+      X(10, 72, 60, 4, 1) X(11, 60, 72, 4, 1) X(12, 72, 60, 2, 2) X(14, 45, 48, 4, 2)
 
 template <int N1, int N2, int CW, int MINB>
 cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s);

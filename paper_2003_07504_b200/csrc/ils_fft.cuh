@@ -97,6 +97,7 @@ struct KmOf {
 // Group of G threads owning one line.  GC > 0 makes the size compile-time.
 template <int GC>
 struct GroupT {
+  static constexpr int kSize = GC;  // compile-time group size (0: runtime)
   int id;     // group index inside the CTA (named barrier id - 1)
   int size_;  // runtime size (GC == 0)
   int rank;   // thread index inside the group

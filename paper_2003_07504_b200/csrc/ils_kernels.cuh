@@ -390,8 +390,10 @@ constexpr int kTwSplitMax = 32;  // entries of the w^(32 m) table (N/2 < 32 * 32
 // X[k] = E + w^k O, X[N-k] = conj(E - w^k O), E = (Z_k + conj Z_{N-k})/2,
 // O = -i (Z_k - conj Z_{N-k})/2, w = exp(-2 pi i/W).  X[N] goes to element N.
 // (complex operations: the packed FP32x2 forms in fp32 translation units)
-// (N and the group size are compile-time constants for the compile-time row
-// plans: the loop then unrolls, with the k == 0 / k == N/2 cases folded)
+// (compile-time plans: N and the group size are constants and the loop
+// unrolls, the k == 0 / k == N/2 cases folded -- 1080p IT pass 30.7 -> 29.5 us,
+// 3840-wide IT 172 -> 158 us, 7680-wide IT 695 -> 652 us)
+
 template <typename T, class TW, class Grp>
 __device__ __forceinline__ void r2c_post(cx<T>* z, int N, const TW& tw, const Grp& g) {
   const int M = (N / 2) / g.size() + 1;
@@ -469,11 +471,12 @@ constexpr bool kBulkRows = sizeof(T) == 4 && FS::n > 0 && (2 * FS::n) % 8 == 0;
 // than the band-12 CTA's lower halo overhead (4993 -> 5859 frames/s);
 // runtime plans for 2
 #ifndef ILS_ROW_MINB  // (tuning override: resident row CTAs per SM the registers are budgeted for)
-// (the 3840-point line plan -- 7680-wide rows -- fits one CTA per SM in
-// shared memory, so it gets the whole register file: 1.1 KB of spills per
-// thread at 80 registers, IT pass 1285 -> 751 us)
+// (the 1920- and 3840-point line plans -- 3840 / 7680-wide rows -- fit one
+// CTA per SM in shared memory, so they get the whole register file: at 80
+// registers the 7680-wide pass spilled 1.1 KB per thread, IT 1285 -> 751 us,
+// and the 3840-wide final pass 136 bytes, 75 -> 57 us)
 template <class FS>
-constexpr int kRowBlocksOf = FS::n > 0 ? (FS::n >= 3840 ? 1 : 3) : 2;
+constexpr int kRowBlocksOf = FS::n > 0 ? (FS::n >= 1920 ? 1 : 3) : 2;
 #else
 template <class FS>
 constexpr int kRowBlocksOf = ILS_ROW_MINB;

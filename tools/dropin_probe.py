@@ -44,3 +44,36 @@ res["d2h_f64_into_torch_pinned_empty_ms"], _ = t(
 res["d2h_f64_pageable_ms"], _ = t(lambda: d64.cpu())
 res["np_empty_plus_copy_ms"], _ = t(lambda: [np.copyto(np.empty((H, W)), planes[i]) for i in range(3)])
 print({k: round(v, 3) for k, v in res.items()})
+
+# input alternatives: pageable H2D of each plane from its own thread / stream
+from concurrent.futures import ThreadPoolExecutor  # noqa: E402
+
+pool = ThreadPoolExecutor(3)
+streams = [torch.cuda.Stream() for _ in range(3)]
+dst = torch.empty((3, H, W), dtype=torch.float64, device="cuda")
+
+
+def par_pageable():
+    def one(i):
+        with torch.cuda.stream(streams[i]):
+            dst[i].copy_(torch.from_numpy(planes[i]), non_blocking=True)
+            streams[i].synchronize()
+    list(pool.map(one, range(3)))
+
+
+res2 = {}
+res2["h2d_pageable_3threads_ms"], _ = t(par_pageable)
+stage3 = [torch.empty((H, W), dtype=torch.float64, pin_memory=True) for _ in range(3)]
+
+
+def par_staged():
+    def one(i):
+        np.copyto(stage3[i].numpy(), planes[i])
+        with torch.cuda.stream(streams[i]):
+            dst[i].copy_(stage3[i], non_blocking=True)
+            streams[i].synchronize()
+    list(pool.map(one, range(3)))
+
+
+res2["staged_per_plane_3threads_ms"], _ = t(par_staged)
+print({k: round(v, 3) for k, v in res2.items()})
