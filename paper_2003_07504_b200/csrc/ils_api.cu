@@ -381,7 +381,7 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
     }
   }
   if (best == 1e300) return false;
-  p.row_threads = kRowThreads;
+  p.row_threads = (spec && p.row_spec >= 0 && spec->n == 960) ? ILS_ROW_THREADS_960 : kRowThreads;
   p.LP = LP;
   p.row_grid = (p.H + p.band - 1) / p.band;
   // rolling-band first / fused passes for the wide compile-time plans: a ring

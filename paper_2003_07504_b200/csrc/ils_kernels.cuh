@@ -451,6 +451,13 @@ struct AddPair {  // element e of a packed line += (f[2e], f[2e+1])
 };
 
 constexpr int kRowThreads = 256;
+// threads per row CTA of a compile-time plan (the 960-point line plan of
+// 1920-wide rows is a tuning point: ILS_ROW_THREADS_960)
+#ifndef ILS_ROW_THREADS_960
+#define ILS_ROW_THREADS_960 256
+#endif
+template <class FS>
+constexpr int kRowThreadsOf = FS::n == 960 ? ILS_ROW_THREADS_960 : kRowThreads;
 constexpr int kColThreads = 256;
 constexpr int kColMinBlocks = 3;  // k_col register budget: 3 CTAs / SM
 constexpr int kNarrowMaxW = 4 * 4 * kRowThreads;  // stencil: 4 strips x 4 columns per thread
@@ -523,7 +530,7 @@ template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 #ifdef ILS_ROW_MAXREG  // (tuning override: explicit register cap for the row kernels)
 __global__ void __maxnreg__(ILS_ROW_MAXREG) k_row(const RowArgs<T> A) {
 #else
-__global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
+__global__ void __launch_bounds__(kRowThreadsOf<FS>, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
 #endif
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[32];
@@ -890,7 +897,7 @@ __global__ void __launch_bounds__(kRowThreads, kRowBlocksOf<FS>) k_row(const Row
     // every strip is whole when the compile-time width is a multiple of QW
     constexpr bool ALLFULL = WCT > 0 && WCT % QW == 0;
     // strips per thread: exact for compile-time plans, 4 (W <= 16 * 256) otherwise
-    constexpr int GMAX = FS::n > 0 ? (2 * FS::n / QW + kRowThreads - 1) / kRowThreads : 4;
+    constexpr int GMAX = FS::n > 0 ? (2 * FS::n / QW + kRowThreadsOf<FS> - 1) / kRowThreadsOf<FS> : 4;
     const int ng = (W + QW - 1) / QW;
     const bool is_it = MODE == MODE_IT;
     T chk = T(0);  // fma(x, 0, chk) turns NaN on any non-finite x

@@ -1,11 +1,7 @@
-# end-of-session validation: the driver's round-end commands, twice for flakiness
+# final check: all GPU tests + smoke, then the full bench line and the reference arm
 mkdir -p gpurun_out
-: > gpurun_out/final.log
-for i in 1 2; do
-  timeout 900 python -m pytest tests -m gpu -x -q >> gpurun_out/final.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final.log
-done
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" >> gpurun_out/final.log 2>&1
-for i in 1 2 3; do
-  timeout 900 python bench.py --no-cpu --no-cufft >> gpurun_out/final.log 2>&1
-done
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 true
