@@ -119,6 +119,16 @@ __device__ __forceinline__ cx<T> ldg_cx(const cx<T>* p) {
   }
 }
 
+// An optimisation barrier on a value: the compiler must assume it changes
+// here, so nothing computed from it can be hoisted above this point.
+template <typename T>
+__device__ __forceinline__ void opaque(cx<T>& w) {
+  if constexpr (sizeof(T) == 4)
+    asm volatile("" : "+f"(w.x), "+f"(w.y));
+  else
+    asm volatile("" : "+d"(w.x), "+d"(w.y));
+}
+
 // Twiddle load pinned between the pass barriers (a plain __ldg of read-only
 // data may be hoisted above every barrier of the transform).
 template <typename T>
@@ -185,6 +195,15 @@ __device__ __forceinline__ void fft_pass(cx<T>* __restrict__ x, int nb, int Ns, 
       // base twiddle: from the per-thread cache (compile-time plans: it only
       // depends on the thread's rank, so it is loaded once per kernel) or the table
       cx<T> w1 = wcache ? wcache[k] : ldtw(tw + (j % Ns));
+#ifndef ILS_TW_HOIST
+      // a cached base is the same for every line the thread transforms: left
+      // visible, nvcc hoists the whole chain of powers out of the caller's
+      // line loop and keeps R-1 complex values per pass live across the
+      // kernel -- spilled to local memory at 3840 / 7680 wide (300 bytes per
+      // thread, reloaded through L2 in every butterfly).  Recomputing the
+      // chain per line is a few FFMA2 per power.
+      if (wcache) opaque(w1);
+#endif
       if (DIR > 0) w1.y = -w1.y;
       if constexpr (R <= 16) {
         cx<T> w = w1;
