@@ -36,8 +36,9 @@ struct Col2Shape {
   static constexpr int NT = (CW * R + 31) / 32 * 32;
   static constexpr int PAD = ((CW * (1 - N2)) % 16 + 16) % 16;
   static constexpr int KS = N2 * CW + PAD;
-  static constexpr int TILE = N1 * KS;  // complex elements
+  static constexpr int TILE = (N1 * KS + 1) & ~1;  // complex elements (whole 16-byte pairs: the tables follow)
   static constexpr size_t SMEM = (size_t)TILE * 8 + (size_t)H * 8 + (size_t)H * 4;
+  static_assert(H % 4 == 0, "the tables arrive by bulk copy: whole 16-byte rows");
 };
 
 // (__launch_bounds__ leaves the 288-thread 30 x 36 strip at 96 registers with
@@ -63,9 +64,17 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
 #ifndef ILS_PDL_LATE
   pdl_trigger();
 #endif
-  for (int m = t; m < H; m += S::NT) {  // constant tables: before the wait on the previous pass
-    stw[m] = ldg_cx(A.tw2 + m);
-    swy[m] = __ldg(A.wy + m);
+  // the constant tables: two bulk copies issued before the wait on the
+  // previous pass, landing while the strip's rows load (a per-thread
+  // load -> store loop costs H / NT serial L2 round trips per CTA: 10% of
+  // the 8K pass)
+  __shared__ unsigned long long tbar;
+  if (t == 0) {
+    mbar_init(&tbar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&tbar, (unsigned)(H * 12));
+    bulk_g2s(stw, A.tw2, (unsigned)(H * 8), &tbar);
+    bulk_g2s(swy, A.wy, (unsigned)(H * 4), &tbar);
   }
   pdl_wait();
   cx<float> v[N1];
@@ -74,7 +83,8 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
     for (int n1 = 0; n1 < N1; ++n1)
       v[n1] = colok ? ldg_cx(Spl + (size_t)(r + N2 * n1) * A.S_rp) : cx<float>{0.f, 0.f};
   }
-  __syncthreads();
+  __syncthreads();  // (also publishes tbar's initialisation)
+  mbar_wait(&tbar, 0);
   if (actA) {
     dft<N1, -1>(v);
     cx<float>* d = buf + r * CW + c;

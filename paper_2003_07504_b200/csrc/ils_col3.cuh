@@ -39,7 +39,7 @@ struct Col3Shape {
   static constexpr int TA = M, TB1 = N1 * N3, TB2 = N1 * N2;
   static constexpr int TMAX = TA > TB1 ? (TA > TB2 ? TA : TB2) : (TB1 > TB2 ? TB1 : TB2);
   static constexpr int NT = (CW * TMAX + 31) / 32 * 32;
-  static constexpr int TILE = H * CW;  // complex elements
+  static constexpr int TILE = (H * CW + 1) & ~1;  // complex elements (whole 16-byte pairs: the tables follow)
   // tile + w_H^m (m < H) + w_M^m (m < M) + wy (H floats)
   static constexpr size_t SMEM = (size_t)TILE * 8 + (size_t)H * 8 + (size_t)M * 8 + (size_t)H * 4;
 };
