@@ -346,9 +346,9 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
   if (p.rowf.swz == 3) LP = std::max(LP, (p.N + p.N / 32 + 1) & ~1);  // padded interior layout
   // packing twiddles staged in shared memory, except for kind-3 plans (L1)
 #ifndef ILS_WREAL_SMEM
-  const size_t wreal_bytes = (p.packed && p.rowf.swz != 3) ? (size_t)(p.N / 2 + 1) * elt : 0;
+  const size_t wreal_bytes = (p.packed && p.rowf.swz != 3) ? (size_t)((p.N / 2 + 2) & ~1) * elt : 0;  // whole pairs
 #else
-  const size_t wreal_bytes = p.packed ? (size_t)(p.N / 2 + 1) * elt : 0;
+  const size_t wreal_bytes = p.packed ? (size_t)((p.N / 2 + 2) & ~1) * elt : 0;
 #endif
   // Band size: minimise (waves x per-CTA work).  A CTA of band b transforms
   // b+2 lines c2r and b lines r2c; k CTAs fit an SM while smem <= 228/k KB

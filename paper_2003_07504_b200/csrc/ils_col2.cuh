@@ -153,10 +153,11 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
 
 // (id, N1, N2, CW, min CTAs per SM); a plan takes the first entry with N1 N2 = H
 // (ILS_COL2_SPEC=id overrides, for sweeps: tools/gpu_sweep_col2.sh,
-// tools/gpu_sweep_band_col2.sh -- with the round-2 row passes 36 x 30 leads
-// 30 x 36 by ~1% in the bench, and it does not spill)
+// tools/gpu_sweep_band_col2.sh, tools/gpu_col2_resweep.sh -- with the tables
+// bulk-copied, 30 x 36 runs a 1080p RGB pass in 19.1 us alone vs 20.3 for
+// 36 x 30, +0.4% in the bench, despite 100 bytes of L1-resident spills)
 #define ILS_COL2_SPECS(X)                                                                                    \
-  X(0, 36, 30, 8, 2) X(5, 30, 36, 8, 2) X(1, 36, 30, 6, 3) X(2, 36, 30, 4, 4) X(3, 36, 30, 10, 1) X(4, 36, 30, 10, 2) \
+  X(5, 30, 36, 8, 2) X(0, 36, 30, 8, 2) X(1, 36, 30, 6, 3) X(2, 36, 30, 4, 4) X(3, 36, 30, 10, 1) X(4, 36, 30, 10, 2) \
       X(6, 36, 30, 16, 1) X(8, 48, 45, 8, 1) X(9, 45, 48, 8, 1) X(7, 48, 45, 4, 2) \
       X(10, 72, 60, 4, 1) X(11, 60, 72, 4, 1) X(12, 72, 60, 2, 2) X(14, 45, 48, 4, 2)
 

@@ -582,9 +582,18 @@ __global__ void __launch_bounds__(kRowThreadsOf<FS>, kRowBlocksOf<FS>) k_row(con
   // kind-3 plans without the table in shared memory: split twiddles
   constexpr bool WSPLIT = !WSMEM && FS::G == 32 && FS::n / 2 / 32 < kTwSplitMax;
   __shared__ cx<T> s_whi[WSPLIT ? kTwSplitMax : 1];
+  // the packing twiddles by one bulk copy (whole 16-byte pairs; the host
+  // sizes the region so), waited for after the PDL wait
+  __shared__ unsigned long long wbar;
   if (PACKED && WSMEM) {
-    for (int k = tid; k <= A.N / 2; k += nthr) swreal[k] = A.wreal[k];
-    __syncthreads();
+    if (tid == 0) {
+      const unsigned wb = (unsigned)(((A.N / 2 + 2) & ~1) * sizeof(cx<T>));
+      mbar_init(&wbar, 1);
+      mbar_fence_init();
+      mbar_expect_tx(&wbar, wb);
+      bulk_g2s(swreal, A.wreal, wb, &wbar);
+    }
+    __syncthreads();  // publishes wbar's initialisation
   }
   if (PACKED && WSPLIT) {
     if (tid * 32 <= A.N / 2) s_whi[tid] = A.wreal[32 * tid];
@@ -609,6 +618,7 @@ __global__ void __launch_bounds__(kRowThreadsOf<FS>, kRowBlocksOf<FS>) k_row(con
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((unsigned)(W * sizeof(T))) : "memory");
   }
   pdl_wait();  // the previous pass's spectrum / the caller's f from here on
+  if (PACKED && WSMEM) mbar_wait(&wbar, 0);
 
   if (MODE == MODE_MU || MODE == MODE_R2C) {
     // rhs rows straight from global memory; each group owns whole lines.

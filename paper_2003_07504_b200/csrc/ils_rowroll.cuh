@@ -73,12 +73,17 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   // (16-byte aligned: float4 strips; the twiddle table is rounded up to whole pairs)
   T* smyup = reinterpret_cast<T*>(reinterpret_cast<cx<T>*>(smem_raw) + (size_t)NS * A.LP +
                                   (WSMEM ? ((A.N / 2 + 2) & ~1) : 0));
-  if (WSMEM)
-    for (int k = tid; k <= A.N / 2; k += kRowThreads) swreal[k] = A.wreal[k];
+  __shared__ unsigned long long wbar;  // the packing twiddles: one bulk copy (whole pairs)
   TwCache<T, FS> twc;
   fill_twcache(twc, A.fft, g);
   if (tid < NS) mbar_init(&bars[tid], 1);
+  if (WSMEM && tid == 0) mbar_init(&wbar, 1);
   mbar_fence_init();
+  if (WSMEM && tid == 0) {
+    const unsigned wb = (unsigned)(((A.N / 2 + 2) & ~1) * sizeof(cx<T>));
+    mbar_expect_tx(&wbar, wb);
+    bulk_g2s(swreal, A.wreal, wb, &wbar);
+  }
   const unsigned spec_bytes = (unsigned)((A.Wc * sizeof(cx<T>) + 15) & ~size_t(15));
   pdl_trigger();
 #ifdef ILS_ROLL_F_PREFETCH  // (tuning: the chunk's f rows into L2 up front -- at 3840 wide the
@@ -89,8 +94,9 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
                    "r"((unsigned)(W * sizeof(T)))
                    : "memory");
 #endif
-  __syncthreads();  // barriers initialised, twiddle table staged
+  __syncthreads();  // barriers initialised
   pdl_wait();
+  if (WSMEM) mbar_wait(&wbar, 0);
 
   // (no lambdas here: a closure capturing the kernel's parameter block by
   // reference makes nvcc copy it to local memory and read every field, the

@@ -76,7 +76,7 @@ def test_hot_sizes_use_compile_time_plans():
     _lib.lib().ils_plan_destroy(p)
 
 
-@pytest.mark.parametrize("h,w,n1n2", [(1080, 1920, (36, 30)), (2160, 3840, (48, 45)), (4320, 7680, (72, 60)),
+@pytest.mark.parametrize("h,w,n1n2", [(1080, 1920, (30, 36)), (2160, 3840, (48, 45)), (4320, 7680, (72, 60)),
                                       (512, 512, None)])
 def test_column_solve_kernel_choice(h, w, n1n2):
     # heights with a two-stage split run k_col2 (fp32); the 1080p row plan is
