@@ -330,9 +330,10 @@ def c4_leg(args, world, rank, dev, barrier, max_over_ranks):
         g.manual_seed(20240607 + mine[i])
         frames[i] = torch.rand((ch, h, w), generator=g, device=dev)
     out = torch.empty_like(frames)
-    # one lane: a 4K frame's passes fill the GPU on their own, and a second
-    # concurrent frame only adds L2 pressure (tools/c4_planes.py: 1013 vs 980 frames/s)
-    nlanes = 1
+    # two lanes (frames i, i+1 concurrently): with the spill-free rolling row
+    # pass, 1252 vs 1180 frames/s for one lane (tools/gpu_shapes2.sh); frames
+    # i and i + nin (nin even) share an output slot and a lane, never both
+    nlanes = int(os.environ.get("ILS_C4_LANES", "2"))
     lanes = [torch.cuda.Stream(device=dev) for _ in range(nlanes)]
     wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev) for _ in lanes]
     sts = [torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev) for _ in lanes]
