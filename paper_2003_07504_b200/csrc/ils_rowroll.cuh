@@ -269,14 +269,18 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
         // the row this slot's next load will fetch, and the f row the next
         // step's r2c adds -- the step's loads then come from L2, not DRAM
         // (3840 / 7680 wide: the planes do not fit L2)
-        const int y2 = jn + NG + 1 + i;
+#ifndef ILS_ROLL_L2PF_STEPS
+#define ILS_ROLL_L2PF_STEPS 1
+#endif
+        const int y2 = jn + ILS_ROLL_L2PF_STEPS * NG + 1 + i;
         if (y2 <= r1) {
           if (IT)
             prefetch_l2(Sin_b + (size_t)wrapi(y2, H) * S_rp, spec_bytes);
           else
             prefetch_l2(fpl + (size_t)wrapi(y2, H) * f_rp, (unsigned)(W * sizeof(T)));
         }
-        if (IT && j + NG + i < r1) prefetch_l2(fpl + (size_t)(j + NG + i) * f_rp, (unsigned)(W * sizeof(T)));
+        if (IT && j + ILS_ROLL_L2PF_STEPS * NG + i < r1)
+          prefetch_l2(fpl + (size_t)(j + ILS_ROLL_L2PF_STEPS * NG + i) * f_rp, (unsigned)(W * sizeof(T)));
 #endif
       }
     }
