@@ -29,7 +29,7 @@
 
 namespace ils {
 
-template <int N1, int N2, int CW>
+template <int N1, int N2, int CW, int MINB>
 struct Col2Shape {
   static constexpr int H = N1 * N2;
   static constexpr int R = N1 > N2 ? N1 : N2;
@@ -37,7 +37,11 @@ struct Col2Shape {
   static constexpr int PAD = ((CW * (1 - N2)) % 16 + 16) % 16;
   static constexpr int KS = N2 * CW + PAD;
   static constexpr int TILE = (N1 * KS + 1) & ~1;  // complex elements (whole 16-byte pairs: the tables follow)
-  static constexpr size_t SMEM = (size_t)TILE * 8 + (size_t)H * 8 + (size_t)H * 4;
+  // the constant tables stay in global memory (read through L1) when staging
+  // them would keep MINB strips from sharing an SM: the 4320-row strip of 2
+  // columns, 69 KB of tile, then fits 2 CTAs per SM with 118 KB of L1 left
+  static constexpr bool TG = ((size_t)TILE * 8 + (size_t)H * 12) * MINB > 227 * 1024;
+  static constexpr size_t SMEM = (size_t)TILE * 8 + (TG ? 0 : (size_t)H * 12);
   static_assert(H % 4 == 0, "the tables arrive by bulk copy: whole 16-byte rows");
 };
 
@@ -45,13 +49,16 @@ struct Col2Shape {
 // 100 bytes of L1-resident spills; an explicit 112-register cap removes them
 // but measured slower, 23.5 vs 19.8 us per 1080p RGB pass)
 template <int N1, int N2, int CW, int MINB>
-__global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const ColArgs<float> A) {
-  using S = Col2Shape<N1, N2, CW>;
+__global__ void __launch_bounds__(Col2Shape<N1, N2, CW, MINB>::NT, MINB) k_col2(const ColArgs<float> A) {
+  using S = Col2Shape<N1, N2, CW, MINB>;
   constexpr int H = S::H, KS = S::KS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cx<float>* buf = reinterpret_cast<cx<float>*>(smem_raw);
   cx<float>* stw = buf + S::TILE;                  // w_H^m = exp(-2 pi i m / H), m < H
   float* swy = reinterpret_cast<float*>(stw + H);  // 2 - 2 cos(2 pi ky / H)
+  // table reads: shared memory, or global through L1 (S::TG)
+#define ILS_C2_TW(m) (S::TG ? ldg_cx(A.tw2 + (m)) : stw[m])
+#define ILS_C2_WY(m) (S::TG ? __ldg(A.wy + (m)) : swy[m])
   const int t = threadIdx.x;
   const int c = t % CW, r = t / CW;
   const int b = blockIdx.y;
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
   // load -> store loop costs H / NT serial L2 round trips per CTA: 10% of
   // the 8K pass)
   __shared__ unsigned long long tbar;
-  if (t == 0) {
+  if (!S::TG && t == 0) {
     mbar_init(&tbar, 1);
     mbar_fence_init();
     mbar_expect_tx(&tbar, (unsigned)(H * 12));
@@ -84,13 +91,13 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
       v[n1] = colok ? ldg_cx(Spl + (size_t)(r + N2 * n1) * A.S_rp) : cx<float>{0.f, 0.f};
   }
   __syncthreads();  // (also publishes tbar's initialisation)
-  mbar_wait(&tbar, 0);
+  if (!S::TG) mbar_wait(&tbar, 0);
   if (actA) {
     dft<N1, -1>(v);
     cx<float>* d = buf + r * CW + c;
     d[0] = v[0];
 #pragma unroll
-    for (int k1 = 1; k1 < N1; ++k1) d[k1 * KS] = cmul(v[k1], stw[r * k1]);
+    for (int k1 = 1; k1 < N1; ++k1) d[k1 * KS] = cmul(v[k1], ILS_C2_TW(r * k1));
   }
   __syncthreads();
 
@@ -106,11 +113,11 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
     const float cl2 = A.cl2_of(b);
     const float base = 1.f + cl2 * __ldg(A.wx + min(c0 + c, A.Wc - 1));
 #pragma unroll
-    for (int k2 = 0; k2 < N2; ++k2) w[k2] = scale(w[k2], fast_div(A.inv_hw, base + cl2 * swy[r + N1 * k2]));
+    for (int k2 = 0; k2 < N2; ++k2) w[k2] = scale(w[k2], fast_div(A.inv_hw, base + cl2 * ILS_C2_WY(r + N1 * k2)));
     dft<N2, +1>(w);
     d[0] = w[0];
 #pragma unroll
-    for (int n2 = 1; n2 < N2; ++n2) d[n2 * CW] = cmulc(w[n2], stw[n2 * r]);
+    for (int n2 = 1; n2 < N2; ++n2) d[n2 * CW] = cmulc(w[n2], ILS_C2_TW(n2 * r));
   }
   __syncthreads();
 
@@ -149,6 +156,8 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
       }
     }
   }
+#undef ILS_C2_TW
+#undef ILS_C2_WY
 }
 
 // (id, N1, N2, CW, min CTAs per SM); a plan takes the first entry with N1 N2 = H
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(Col2Shape<N1, N2, CW>::NT, MINB) k_col2(const 
 #define ILS_COL2_SPECS(X)                                                                                    \
   X(5, 30, 36, 8, 2) X(0, 36, 30, 8, 2) X(1, 36, 30, 6, 3) X(2, 36, 30, 4, 4) X(3, 36, 30, 10, 1) X(4, 36, 30, 10, 2) \
       X(6, 36, 30, 16, 1) X(8, 48, 45, 8, 1) X(9, 45, 48, 8, 1) X(7, 48, 45, 4, 2) \
-      X(10, 72, 60, 4, 1) X(11, 60, 72, 4, 1) X(12, 72, 60, 2, 2) X(14, 45, 48, 4, 2)
+      X(10, 72, 60, 4, 1) X(11, 60, 72, 4, 1) X(12, 72, 60, 2, 2) X(14, 45, 48, 4, 2) X(15, 60, 72, 2, 2)
 
 template <int N1, int N2, int CW, int MINB>
 cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s);
@@ -167,7 +176,7 @@ cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s
 #ifdef ILS_DEFINE_LAUNCHERS
 template <int N1, int N2, int CW, int MINB>
 cudaError_t launch_col2_impl(const ColArgs<float>& a, int planes, cudaStream_t s) {
-  using S = Col2Shape<N1, N2, CW>;
+  using S = Col2Shape<N1, N2, CW, MINB>;
   auto k = k_col2<N1, N2, CW, MINB>;
   cudaError_t e = smem_attr(reinterpret_cast<const void*>(k), S::SMEM);
   if (e != cudaSuccess) return e;
