@@ -91,9 +91,11 @@ def main(rep, out_txt, what="one 1080p RGB frame", traffic_name="traffic.json"):
             tag = "k_row_roll_it" if ", 1, " in k else "k_row_roll_f0"
             agg.setdefault(tag, []).append(d)
             continue
-        tag = ("k_row_it" if ", 1>" in k or k.endswith("1>") else
-               "k_row_f0" if k.endswith("0>") else "k_row_fin" if k.endswith("3>") else
-               "k_col2" if "k_col2" in k else "k_col" if "k_col" in k else None)
+        if "k_col" in k:
+            tag = "k_col2" if "k_col2" in k else "k_col3" if "k_col3" in k else "k_col"
+        else:
+            tag = ("k_row_it" if ", 1>" in k or k.endswith("1>") else
+                   "k_row_f0" if k.endswith("0>") else "k_row_fin" if k.endswith("3>") else None)
         if tag is None:
             continue
         agg.setdefault(tag, []).append(d)
