@@ -690,9 +690,45 @@ def main():
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + (F // G) * 4,
                 "ms_per_step": round(ms_e2e, 3), "api": api}
 
+    def pcie_link(nbytes):
+        """Pinned copies of one frame's bytes on this box: H2D alone, D2H alone, and both
+        directions at once (the e2e pipeline's steady state), GB/s per direction."""
+        hs = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        hd = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        ds = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        dd = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        reps = 20
+
+        def timed(h2d, d2h):
+            torch.cuda.synchronize()
+            a = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            a[0].record(s1)
+            a[2].record(s2)
+            for _ in range(reps):
+                if h2d:
+                    with torch.cuda.stream(s1):
+                        ds.copy_(hs, non_blocking=True)
+                if d2h:
+                    with torch.cuda.stream(s2):
+                        hd.copy_(dd, non_blocking=True)
+            a[1].record(s1)
+            a[3].record(s2)
+            torch.cuda.synchronize()
+            ms = max(a[0].elapsed_time(a[1]) if h2d else 0.0, a[2].elapsed_time(a[3]) if d2h else 0.0)
+            return nbytes * reps / (ms / 1e3) / 1e9
+
+        timed(True, True)
+        h2d, d2h, both = timed(True, False), timed(False, True), timed(True, True)
+        return {"h2d_GBps": round(h2d, 1), "d2h_GBps": round(d2h, 1), "both_directions_GBps_each": round(both, 1),
+                "frames_per_s_bound": round(both * 1e9 / nbytes, 1), "bytes_per_frame_each_way": nbytes,
+                "note": "pinned copies of one frame's 8-bit bytes in 20 reps; the e2e pipeline moves each "
+                        "frame both ways at once, so the concurrent figure bounds e2e"}
+
     e2e = e2e_f32 = None
     if not args.no_e2e:
         e2e = e2e_leg(u8=True)
+        e2e["pcie"] = pcie_link(CH * H * W)
         e2e_f32 = e2e_leg(u8=False)
 
     # ---- comparison: the same loop on cuFFT + torch elementwise, same frames
