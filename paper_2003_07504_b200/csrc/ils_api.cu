@@ -282,6 +282,8 @@ struct ils_plan {
   ils_params prm;
   int band, row_threads, row_grid, LP;
   size_t row_smem;
+  int fin_band = 0;     // rows per CTA of the final pass without trace (no halo)
+  size_t fin_smem = 0;  // its shared memory
   int C, CS, col_threads, col_grid;
   bool col_wide = false;  // k_col<FftRtWide>: 512 threads, one group per line
   size_t col_smem;
@@ -381,6 +383,37 @@ bool choose_row(ils_plan& p, int maxe, size_t elt) {
     }
   }
   if (best == 1e300) return false;
+  // the final pass (no stencil, no halo rows) of the 3840 / 7680-wide plans:
+  // registers budgeted for ILS_FIN_MINB CTAs per SM (kRowBlocksOfMode), so
+  // pick its own row count per CTA that lets them share an SM
+  p.fin_band = p.band + 2;
+  p.fin_smem = p.row_smem;
+  if (spec && p.row_spec >= 0 && spec->n >= 1920 && ILS_FIN_MINB > 1) {
+    // cost ~ waves x (rows + 1) per CTA; among the rows counts within 8% of
+    // the best, the smallest: a smaller CTA co-resides better with the other
+    // lane's passes (4K, two lanes: 4 rows 1301 frames/s, 6 rows 1190)
+    std::vector<double> cost(p.band + 3, 1e300);
+    std::vector<size_t> smems(p.band + 3, 0);
+    double fbest = 1e300;
+    const int forced = env_int("ILS_FIN_BAND", 0);  // (tuning)
+    for (int L = 1; L <= p.band + 2; ++L) {
+      if (forced && L != std::min(forced, p.band + 2)) continue;
+      const size_t sm = (size_t)L * LP * elt + wreal_bytes;
+      const int per_sm = (int)std::min<size_t>(ILS_FIN_MINB, (228 * 1024) / (sm + 1024));
+      if (per_sm < 1) break;
+      const long slots = (long)p.sms * per_sm;
+      const long ctas = (long)p.B * ((p.H + L - 1) / L);
+      cost[L] = (double)((ctas + slots - 1) / slots) * (L + 1.0);
+      smems[L] = sm;
+      fbest = std::min(fbest, cost[L]);
+    }
+    for (int L = 1; L <= p.band + 2; ++L)
+      if (cost[L] <= 1.08 * fbest) {
+        p.fin_band = L;
+        p.fin_smem = smems[L];
+        break;
+      }
+  }
   p.row_threads = (spec && p.row_spec >= 0 && spec->n == 960) ? ILS_ROW_THREADS_960 : kRowThreads;
   p.LP = LP;
   p.row_grid = (p.H + p.band - 1) / p.band;
@@ -612,9 +645,11 @@ cudaError_t launch_row(const ils_plan* p, int mode, RowArgs<T> a, cudaStream_t s
   // band's 2 halo line slots with 2 more rows of its own (same shared memory,
   // one CTA transforms band + 2 lines in the same round of line groups)
   int gx = p->row_grid;
+  size_t smem = p->row_smem;
   if (mode == MODE_FIN && a.epart == nullptr) {
-    a.band = p->band + 2;
+    a.band = p->fin_band;
     gx = (p->H + a.band - 1) / a.band;
+    smem = p->fin_smem;
   }
   const dim3 grid(gx, p->B);
   if constexpr (std::is_same<T, float>::value) {
@@ -639,16 +674,16 @@ cudaError_t launch_row(const ils_plan* p, int mode, RowArgs<T> a, cudaStream_t s
     switch (p->row_spec) {
 #define ILS_CASE(ID, ...) \
   case ID:                \
-    return launch_row_impl<float, true, RowSpec<ID>::type, ILS_ROW_SPEC_WIDE(ID)>(a, grid, p->row_threads, p->row_smem, s);
+    return launch_row_impl<float, true, RowSpec<ID>::type, ILS_ROW_SPEC_WIDE(ID)>(a, grid, p->row_threads, smem, s);
       ILS_ROW_SPECS(ILS_CASE)
 #undef ILS_CASE
       default:
         break;
     }
   }
-  if (p->W > kNarrowMaxW) return launch_row_impl<T, true, FftRt, true>(a, grid, p->row_threads, p->row_smem, s);
-  return p->packed ? launch_row_impl<T, true, FftRt>(a, grid, p->row_threads, p->row_smem, s)
-                   : launch_row_impl<T, false, FftRt>(a, grid, p->row_threads, p->row_smem, s);
+  if (p->W > kNarrowMaxW) return launch_row_impl<T, true, FftRt, true>(a, grid, p->row_threads, smem, s);
+  return p->packed ? launch_row_impl<T, true, FftRt>(a, grid, p->row_threads, smem, s)
+                   : launch_row_impl<T, false, FftRt>(a, grid, p->row_threads, smem, s);
 }
 
 template <typename T>

@@ -530,11 +530,19 @@ constexpr int kU8Modes = 8;
 #endif
 constexpr int kStencilRows = ILS_STENCIL_ROWS;  // SMODE = kU8Modes + MODE_FIN: 8-bit frame egress
 
+// resident CTAs per SM the registers are budgeted for, per pass kind
+#ifndef ILS_FIN_MINB  // (the 3840 / 7680-wide final pass: 2 CTAs per SM, 114-127 registers, no spills)
+#define ILS_FIN_MINB 2
+#endif
+template <class FS, int SMODE>
+constexpr int kRowBlocksOfMode =
+    (FS::n >= 1920 && (SMODE == MODE_FIN || SMODE == kU8Modes + MODE_FIN)) ? ILS_FIN_MINB : kRowBlocksOf<FS>;
+
 template <typename T, bool PACKED, class FS, bool WIDE, int SMODE>
 #ifdef ILS_ROW_MAXREG  // (tuning override: explicit register cap for the row kernels)
 __global__ void __maxnreg__(ILS_ROW_MAXREG) k_row(const RowArgs<T> A) {
 #else
-__global__ void __launch_bounds__(kRowThreadsOf<FS>, kRowBlocksOf<FS>) k_row(const RowArgs<T> A) {
+__global__ void __launch_bounds__(kRowThreadsOf<FS>, kRowBlocksOfMode<FS, SMODE>) k_row(const RowArgs<T> A) {
 #endif
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[32];

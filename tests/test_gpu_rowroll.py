@@ -94,3 +94,18 @@ def test_traced_and_8bit_calls_keep_k_row_and_agree(monkeypatch):
     ut, st, _, en = _smooth(f, params, monkeypatch, True, trace=True)
     assert st == _lib.STATUS_CLEAN and torch.equal(ur, ut)
     assert torch.all(en[1:] <= en[:-1] * (1 + 1e-6))
+
+
+@pytest.mark.parametrize("H,W", [(333, 3840), (97, 7680)])
+def test_final_pass_rows_per_cta_do_not_change_bits(H, W, monkeypatch):
+    # the wide plans' final pass (c2r -> u, no halo) picks its own rows per CTA
+    # (2 CTAs/SM); every choice must give the same bits
+    params = ils.SmoothParams(ils.Welsch(10 / 255), 30.0, iters=3, c=2.0)
+    f = torch.from_numpy(np.random.default_rng(H).random((2, H, W))).to("cuda", torch.float32)
+    monkeypatch.delenv("ILS_FIN_BAND", raising=False)
+    u0, s0, _, _ = _smooth(f, params, monkeypatch, True)
+    assert s0 == _lib.STATUS_CLEAN
+    for L in (1, 2, 3, 7):
+        monkeypatch.setenv("ILS_FIN_BAND", str(L))
+        u, s, _, _ = _smooth(f, params, monkeypatch, True)
+        assert s == _lib.STATUS_CLEAN and torch.equal(u, u0), L
