@@ -531,13 +531,50 @@ def main():
     lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(S - 1)]
     ps = H * W
 
+    # the ils_smooth pass order through the per-pass entry (ils_launch_pass):
+    # 0 = first row pass, 1 = column pass, 2 = fused row pass, 3 = final row
+    # pass; | 4 = spectrum B is the current one
+    pass_order = [0, 1]
+    for n in range(1, ITERS):
+        cur = 0 if n % 2 else 4
+        pass_order += [2 | cur, 1 | (cur ^ 4)]
+    pass_order += [3 | (0 if ITERS % 2 else 4)]
+    # lane k starts once lane 0 has queued STAGGER * k passes of its first
+    # frame (that frame through ils_launch_pass, the rest through ils_smooth):
+    # lanes in lockstep run the same pass kind at the same time and drain
+    # their tails together; two passes apart measured +1.6% (one or three
+    # apart, a row pass beside a column pass, -0.2 to -2%: tools/stagger_probe.py)
+    stagger = int(os.environ.get("ILS_BENCH_STAGGER", "2"))
+    # that frame's own status word (ils_launch_pass does not reset it; only
+    # lowered by the kernels, checked with the others after the timed region)
+    stat_pp = torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev)
+
     def step_launches(s):
         # frame groups round-robin over S lanes forked from / joined to `s`
-        for ln in lanes[1:]:
-            ln.wait_stream(s)
+        gate = {}
+        if stagger > 0 and S > 1:
+            for k in range(1, S):
+                if stagger * k <= len(pass_order):
+                    gate[stagger * k] = lanes[k]
+                else:
+                    lanes[k].wait_stream(s)
+        else:
+            for ln in lanes[1:]:
+                ln.wait_stream(s)
         for gi, g0 in enumerate(range(0, F, G)):
             k = gi % S
             off = g0 * CH * ps * 4
+            if gi == 0 and gate:
+                for i, p in enumerate(pass_order):
+                    _lib.check(L.ils_launch_pass(plan.ptr, p, C.c_void_p(f.data_ptr() + off),
+                                                 C.c_void_p(u.data_ptr() + off), ps, C.c_void_p(wss[0].data_ptr()),
+                                                 C.c_void_p(s.cuda_stream), C.c_void_p(stat_pp.data_ptr())),
+                               "ils_launch_pass")
+                    if i + 1 in gate:
+                        ev = torch.cuda.Event()
+                        ev.record(s)
+                        gate[i + 1].wait_event(ev)
+                continue
             _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f.data_ptr() + off), C.c_void_p(u.data_ptr() + off), ps,
                                     C.c_void_p(wss[k].data_ptr()), C.c_void_p((s if k == 0 else lanes[k]).cuda_stream),
                                     C.c_void_p(stats[k].data_ptr()), None), "ils_smooth")
@@ -554,7 +591,7 @@ def main():
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
-    for st_ in stats:
+    for st_ in stats + [stat_pp]:
         rt.raise_status(int(st_.item()))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -566,7 +603,7 @@ def main():
             e1.record(stream)
         barrier()
     ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    for st_ in stats:
+    for st_ in stats + [stat_pp]:
         rt.raise_status(int(st_.item()))
     value = world * F / (ms_step / 1e3)
     launches = args.steps * (F // G) * plan.info["launches_per_call"]
@@ -838,7 +875,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": config_of(world),
-            "step": {"frames_per_step_per_gpu": F, "frames_per_launch_group": G, "streams": S},
+            "step": {"frames_per_step_per_gpu": F, "frames_per_launch_group": G, "streams": S,
+                     "lane_stagger_passes": stagger if S > 1 else 0},
             "plan": {k: plan.info[k] for k in ("row_band", "row_group", "row_radix", "row_spec", "col2_spec",
                                                "col2_n1", "col2_n2", "col2_cols")},
             "e2e": e2e,
