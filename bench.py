@@ -61,6 +61,17 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 H, W, CH, ITERS = 1080, 1920, 3, 4
+
+
+def pass_order_of(iters):
+    """The ils_smooth pass order through the per-pass entry (ils_launch_pass):
+    0 = first row pass, 1 = column pass, 2 = fused row pass, 3 = final row
+    pass; | 4 = spectrum B is the current one."""
+    order = [0, 1]
+    for n in range(1, iters):
+        cur = 0 if n % 2 else 4
+        order += [2 | cur, 1 | (cur ^ 4)]
+    return order + [3 | (0 if iters % 2 else 4)]
 P_EXP, EPS, LAM = 0.8, 1e-4, 1.0
 METRIC = "1080p colour ILS frames/s (4 iters) on 1/2/4/8 B200; HBM roofline fraction"
 WORKLOAD = "C3: 1920x1080 RGB ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters"
@@ -338,13 +349,32 @@ def c4_leg(args, world, rank, dev, barrier, max_over_ranks):
     wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev) for _ in lanes]
     sts = [torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev) for _ in lanes]
 
+    # (ILS_C4_STAGGER=k: lane 1 k passes behind lane 0 as in the C3 step --
+    # at 4K it measured slower, 1282 vs 1300 frames/s for k = 2 or 4)
+    stagger = int(os.environ.get("ILS_C4_STAGGER", "0")) if nlanes == 2 else 0
+    order = pass_order_of(ITERS)
+    st_pp = torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev)
+
     def run_all():
         cur = torch.cuda.current_stream(dev)
-        for ln in lanes:
-            ln.wait_stream(cur)
+        lanes[0].wait_stream(cur)
+        if not stagger:
+            for ln in lanes[1:]:
+                ln.wait_stream(cur)
         for i in range(len(mine)):
             k = i % nlanes
             j = i % nin
+            if i == 0 and stagger:
+                for q, p in enumerate(order):
+                    _lib.check(L.ils_launch_pass(plan.ptr, p, C.c_void_p(frames[j].data_ptr()),
+                                                 C.c_void_p(out[j].data_ptr()), h * w, C.c_void_p(wss[0].data_ptr()),
+                                                 C.c_void_p(lanes[0].cuda_stream), C.c_void_p(st_pp.data_ptr())),
+                               "ils_launch_pass")
+                    if q + 1 == stagger:
+                        ev = torch.cuda.Event()
+                        ev.record(lanes[0])
+                        lanes[1].wait_event(ev)
+                continue
             _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(frames[j].data_ptr()), C.c_void_p(out[j].data_ptr()), h * w,
                                     C.c_void_p(wss[k].data_ptr()), C.c_void_p(lanes[k].cuda_stream),
                                     C.c_void_p(sts[k].data_ptr()), None), "ils_smooth")
@@ -361,7 +391,7 @@ def c4_leg(args, world, rank, dev, barrier, max_over_ranks):
     e1.record()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / reps)
-    for st in sts:
+    for st in sts + [st_pp]:
         rt.raise_status(int(st.item()))
     # placement invariance: frame 0 of this rank smoothed alone equals its batch result
     alone = ils.smooth_batch(frames[0], prm)
@@ -374,7 +404,7 @@ def c4_leg(args, world, rank, dev, barrier, max_over_ranks):
     return {"workload": "C4: 3840x2160 RGB video, 256 frames, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
             "value": round(fps, 2), "unit": "frames/s", "frames": args.c4_frames, "n_gpus": world,
             "scaling": "strong (fixed 256-frame batch split over the ranks, no communication)",
-            "ms_per_batch": round(ms, 3), "lanes": nlanes,
+            "ms_per_batch": round(ms, 3), "lanes": nlanes, "lane_stagger_passes": stagger,
             "whole_path": {"achieved": round(bpf * fps / world / 1e9, 1),
                                                          "frac": round(bpf * fps / world / 1e9 / peak, 4),
                                                          "bytes_per_frame": bpf},
@@ -531,14 +561,7 @@ def main():
     lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(S - 1)]
     ps = H * W
 
-    # the ils_smooth pass order through the per-pass entry (ils_launch_pass):
-    # 0 = first row pass, 1 = column pass, 2 = fused row pass, 3 = final row
-    # pass; | 4 = spectrum B is the current one
-    pass_order = [0, 1]
-    for n in range(1, ITERS):
-        cur = 0 if n % 2 else 4
-        pass_order += [2 | cur, 1 | (cur ^ 4)]
-    pass_order += [3 | (0 if ITERS % 2 else 4)]
+    pass_order = pass_order_of(ITERS)
     # lane k starts once lane 0 has queued STAGGER * k passes of its first
     # frame (that frame through ils_launch_pass, the rest through ils_smooth):
     # lanes in lockstep run the same pass kind at the same time and drain
