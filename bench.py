@@ -277,10 +277,27 @@ def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
     wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev) for _ in lanes]
     sts = [torch.empty(1, dtype=torch.int32, device=dev) for _ in lanes]
 
+    # (ILS_GRAY_STAGGER=k: lane 1 k passes behind lane 0 as in the C3 step --
+    # slower for gray frames: C1 28.7k vs 30.7k, C2 12.99k vs 13.15k frames/s at k = 2)
+    stagger = int(os.environ.get("ILS_GRAY_STAGGER", "0"))
+    order = pass_order_of(ITERS)
+    st_pp = torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev)
+
     def launches(s):
-        lanes[1].wait_stream(s)
+        if not stagger:
+            lanes[1].wait_stream(s)
         for k in range(F):
             ln = k % 2
+            if k == 0 and stagger:
+                for q, p in enumerate(order):
+                    _lib.check(L.ils_launch_pass(plan.ptr, p, C.c_void_p(f[0].data_ptr()), C.c_void_p(u[0].data_ptr()),
+                                                 h * w, C.c_void_p(wss[0].data_ptr()), C.c_void_p(s.cuda_stream),
+                                                 C.c_void_p(st_pp.data_ptr())), "ils_launch_pass")
+                    if q + 1 == stagger:
+                        ev = torch.cuda.Event()
+                        ev.record(s)
+                        lanes[1].wait_event(ev)
+                continue
             _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f[k].data_ptr()), C.c_void_p(u[k].data_ptr()), h * w,
                                     C.c_void_p(wss[ln].data_ptr()), C.c_void_p((s if ln == 0 else lanes[1]).cuda_stream),
                                     C.c_void_p(sts[ln].data_ptr()), None), "ils_smooth")
@@ -304,13 +321,14 @@ def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
         e1.record(lanes[0])
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps)
-    for st in sts:
+    for st in sts + [st_pp]:
         rt.raise_status(int(st.item()))
     fps = world * F / (ms / 1e3)
     peak, _ = peaks()
     bpf = bytes_per_frame(ITERS, h, w, 1)
     return {"workload": f"{label}: {w}x{h} gray ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
             "value": round(fps, 1), "unit": "frames/s", "frames_per_step_per_gpu": F, "lanes": 2,
+            "lane_stagger_passes": stagger,
             "whole_path": {"achieved": round(bpf * fps / world / 1e9, 1),
                            "frac": round(bpf * fps / world / 1e9 / peak, 4), "bytes_per_frame": bpf}}
 
