@@ -12,7 +12,13 @@ the iterations, by design.  Frames shard across ranks with no communication
 (scaling "weak").
 
 value     device throughput: frames/s over all ranks, inputs resident in HBM,
-          one CUDA-graph replay per step, CUDA events, max over ranks.
+          one CUDA-graph replay per step, CUDA events, max over ranks.  The
+          frames go round-robin over two lanes (graph branches); lane 1
+          starts two passes after lane 0 (ILS_BENCH_STAGGER), so the lanes
+          do not run in lockstep.
+e2e.pcie  the box's pinned copy rates for one frame's bytes (H2D, D2H, both
+          at once): the e2e path's H2D stream is busy ~100% of the time
+          (tools/host_pipe_probe.py), so the link under kernel load bounds it.
 e2e       the same through the C ABI with HOST buffers (ils_smooth_host_u8):
           pinned host 8-bit RGB frames (the reference's PNG/PPM pixel format)
           -> device copies, kernels (v/255 deinterleave ahead of the first
