@@ -458,6 +458,102 @@ def to_host_f64(t):
     return out
 
 
+def _side_streams(dev):
+    """Per-thread (staging, result) streams of device `dev` for smooth_planes_host."""
+    torch = _torch()
+    cache = getattr(_tls, "side", None)
+    if cache is None:
+        cache = _tls.side = {}
+    key = _dev_index(torch, dev)
+    if key not in cache:
+        cache[key] = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
+    return cache[key]
+
+
+def smooth_planes_host(planes, cparams, precision=None):
+    """Host float64 planes -> smoothed float64 planes, pipelined plane by plane.
+
+    The reference's smooth_color smooths its channels independently
+    (smoother.py:204-213), so each plane can start as soon as its own rows
+    are staged: the chunk copies of all planes run on the host pool and
+    their H2Ds on a staging stream; plane i's smooth (one launch sequence on
+    the caller's stream) waits only for plane i's chunks, and its result
+    widens on the device and goes to pooled pinned memory on a third stream
+    while the next plane computes.  The arithmetic is exactly the batched
+    path's (a plane's bits do not depend on its batch).  Returns None when
+    the pinned result pool is over its cap (the caller uses the batched path).
+    """
+    torch = _torch()
+    dt = torch_dtype(precision)
+    arrs = [np.asarray(p, dtype=np.float64) for p in planes]
+    B = len(arrs)
+    H, W = arrs[0].shape
+    n = B * H * W
+    buf = _out_pool.take(n)
+    if buf is None:
+        return None
+    cur = torch.cuda.current_stream()
+    dev = cur.device
+    s_in, s_out = _side_streams(dev)
+    s_in.wait_stream(cur)
+    narrow = dt == torch.float32 and _HOST_NARROW
+    sdt = dt if narrow else torch.float64
+    stage = _pinned("pipe_in", (B, H, W), sdt)
+    host = stage.numpy()
+    dev_in = torch.empty((B, H, W), dtype=sdt, device=dev)
+    chunks = _row_chunks(B, H, W, 4 if narrow else 8)
+
+    def one(k):
+        i, r0, r1 = chunks[k]
+        np.copyto(host[i, r0:r1], arrs[i][r0:r1], casting="same_kind")
+        with torch.cuda.stream(s_in):
+            dev_in[i, r0:r1].copy_(stage[i, r0:r1], non_blocking=True)
+
+    pool = _host_pool()
+    futs = [pool.submit(one, k) for k in range(len(chunks))]
+    out = buf[:n].view(B, H, W)
+    L = _lib.lib()
+    keep, statuses = [], []
+    try:
+        for i in range(B):
+            for f, (pi, _, _) in zip(futs, chunks):
+                if pi == i:
+                    f.result()
+            ev = torch.cuda.Event()
+            ev.record(s_in)  # after every H2D of plane i (queued by now)
+            cur.wait_event(ev)
+            fi = dev_in[i:i + 1]
+            if sdt != dt:  # staged as f64: narrowed by the library's own kernel
+                f32 = torch.empty((1, H, W), dtype=dt, device=dev)
+                _lib.check(L.ils_convert(C.c_void_p(fi.data_ptr()), _lib.ILS_F64, C.c_void_p(f32.data_ptr()),
+                                         _lib.ILS_F32, H * W, _stream_ptr(torch, dev)), "ils_convert")
+                fi = f32
+            u, _, st = smooth_device(fi, cparams, check=False)
+            statuses.append(st)
+            if u.dtype == torch.float64:
+                w = u
+            else:
+                w = torch.empty((1, H, W), dtype=torch.float64, device=dev)
+                _lib.check(L.ils_convert(C.c_void_p(u.data_ptr()), _lib.ILS_F32, C.c_void_p(w.data_ptr()),
+                                         _lib.ILS_F64, H * W, _stream_ptr(torch, dev)), "ils_convert")
+            done = torch.cuda.Event()
+            done.record(cur)
+            s_out.wait_event(done)
+            with torch.cuda.stream(s_out):
+                out[i:i + 1].copy_(w, non_blocking=True)
+            keep.append((fi, u, w))  # alive until the result stream is drained
+    finally:
+        for f in futs:
+            f.result()
+        s_out.synchronize()
+        cur.synchronize()
+        _pinned_done("pipe_in", s_in)
+    arr = np.asarray(_Lease(buf, (B, H, W)))
+    for st in statuses:  # in plane order, as the batched path reports them
+        raise_status(int(st.item()))
+    return [arr[i] for i in range(B)]
+
+
 def smooth_device_u8(frames, cparams, precision=None, check=True):
     """8-bit interleaved frames uint8[F, H, W, C] on the GPU -> same layout (ils_smooth_u8).
 

@@ -184,8 +184,10 @@ def smooth_color(img: MultiImage, params: SmoothParams, trace: bool = False, wor
                  *, precision: str | None = None):
     """Smooth a gray or RGB image (smoother.py:175-217). Returns image or (image, trace).
 
-    PER_CHANNEL_RGB: the three channels are one batch of one launch sequence
-    (shared plan); traced energies are summed over channels in channel order.
+    PER_CHANNEL_RGB: the channels are staged, smoothed and returned plane by
+    plane in a pipeline (rt.smooth_planes_host); with trace=True they are one
+    batch of one launch sequence and the energies are summed over channels
+    in channel order.
     LUMINANCE_ONLY: BT.601 conversion, Y smoothed, inverse conversion, all on
     the GPU.  Output is not clipped.
     """
@@ -198,8 +200,14 @@ def smooth_color(img: MultiImage, params: SmoothParams, trace: bool = False, wor
         if trace:
             return _image_like(img, (res[0],), GRAY), res[1]
         return _image_like(img, (res,), GRAY)
-    planes = rt.to_device_planes(img.channels, precision)
     cp = params_of(params)
+    if not trace and not is_luminance_only(params):
+        # the channels are independent (smoother.py:204-213): staged, smoothed
+        # and returned plane by plane in a pipeline (same bits as the batch)
+        res = rt.smooth_planes_host(img.channels, cp, precision)
+        if res is not None:
+            return _image_like(img, res, RGB)
+    planes = rt.to_device_planes(img.channels, precision)
     if is_luminance_only(params):
         rt.rgb_yuv_(planes, inverse=False)
         u, en, _ = rt.smooth_device(planes[0:1], cp, trace=trace, check=True)

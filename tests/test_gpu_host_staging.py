@@ -124,3 +124,33 @@ def test_host_narrowing_variant_is_bitwise_the_device_cast(monkeypatch):
     b = ils.smooth_color(img, PARAMS)
     for c in range(3):
         assert np.array_equal(a.channels[c], b.channels[c])
+
+
+def test_pipelined_planes_equal_the_batched_path(monkeypatch):
+    # smooth_color's per-channel pipeline (one launch sequence per plane,
+    # staged and returned plane by plane) gives the batched path's bits
+    rng = np.random.default_rng(9)
+    planes = [rng.random((270, 480)) for _ in range(3)]
+    img = ils.MultiImage(tuple(planes), ils.RGB)
+    piped = ils.smooth_color(img, PARAMS)
+    monkeypatch.setattr(rt, "smooth_planes_host", lambda *a, **k: None)  # force the batched path
+    batched = ils.smooth_color(img, PARAMS)
+    for c in range(3):
+        assert np.array_equal(piped.channels[c], batched.channels[c])
+    monkeypatch.undo()
+    monkeypatch.setattr(rt, "_HOST_NARROW", False)
+    piped64 = ils.smooth_color(img, PARAMS)  # staged as f64, narrowed on the device
+    for c in range(3):
+        assert np.array_equal(piped64.channels[c], batched.channels[c])
+    fp64 = ils.smooth_color(img, PARAMS, precision="fp64")
+    ref = ils.smooth_batch(torch.from_numpy(np.stack(planes)).to("cuda"), PARAMS).cpu().numpy()
+    for c in range(3):
+        assert np.array_equal(fp64.channels[c], ref[c])
+
+
+def test_pipelined_planes_report_errors_in_channel_order():
+    rng = np.random.default_rng(10)
+    huge = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1e30, iters=3)
+    planes = [rng.random((64, 96)) * 1e30 for _ in range(3)]
+    with pytest.raises(ils.NumericalError):
+        ils.smooth_color(ils.MultiImage(tuple(planes), ils.RGB), huge)
