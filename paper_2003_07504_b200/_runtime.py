@@ -252,7 +252,7 @@ _pool = None
 _HOST_THREADS = int(os.environ.get("ILS_HOST_THREADS", "0")) or min(8, os.cpu_count() or 1)
 # staging chunk: small enough that the first DMA starts early, large enough
 # that per-copy launch cost stays negligible
-_CHUNK_BYTES = 4 << 20
+_CHUNK_BYTES = int(float(os.environ.get("ILS_CHUNK_MB", "4")) * (1 << 20))
 # fp32 targets: narrow f64 -> f32 in the staging copy (numpy's cast rounds to
 # nearest-even exactly like the device's ils_convert, tests/test_gpu_host_staging.py)
 # -- half the bytes over PCIe and half the pinned writes: 1080p RGB staging
