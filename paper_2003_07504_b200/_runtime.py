@@ -431,15 +431,19 @@ def to_host_f64(t):
     stream = torch.cuda.current_stream(t.device)
     buf = _out_pool.take(B * H * W) if t.is_contiguous() else None
     if buf is not None:
-        if t.dtype == torch.float64:
-            w = t
-        else:
-            w = torch.empty((B, H, W), dtype=torch.float64, device=t.device)
-            _lib.check(_lib.lib().ils_convert(C.c_void_p(t.data_ptr()), _lib.ILS_F32, C.c_void_p(w.data_ptr()),
-                                              _lib.ILS_F64, t.numel(), _stream_ptr(torch, t.device)),
-                       "ils_convert")
-        buf[:B * H * W].view(B, H, W).copy_(w, non_blocking=True)
-        stream.synchronize()  # the caller reads the arrays next: nothing left in flight
+        try:
+            if t.dtype == torch.float64:
+                w = t
+            else:
+                w = torch.empty((B, H, W), dtype=torch.float64, device=t.device)
+                _lib.check(_lib.lib().ils_convert(C.c_void_p(t.data_ptr()), _lib.ILS_F32, C.c_void_p(w.data_ptr()),
+                                                  _lib.ILS_F64, t.numel(), _stream_ptr(torch, t.device)),
+                           "ils_convert")
+            buf[:B * H * W].view(B, H, W).copy_(w, non_blocking=True)
+            stream.synchronize()  # the caller reads the arrays next: nothing left in flight
+        except BaseException:
+            _out_pool.give(buf)
+            raise
         arr = np.asarray(_Lease(buf, (B, H, W)))
         return [arr[i] for i in range(B)]
     # past the cap: fresh arrays, widened on the host in row chunks
@@ -514,6 +518,7 @@ def smooth_planes_host(planes, cparams, precision=None):
     out = buf[:n].view(B, H, W)
     L = _lib.lib()
     keep, statuses = [], []
+    ok = False
     try:
         for i in range(B):
             for f, (pi, _, _) in zip(futs, chunks):
@@ -542,12 +547,15 @@ def smooth_planes_host(planes, cparams, precision=None):
             with torch.cuda.stream(s_out):
                 out[i:i + 1].copy_(w, non_blocking=True)
             keep.append((fi, u, w))  # alive until the result stream is drained
+        ok = True
     finally:
         for f in futs:
-            f.result()
+            f.exception()  # wait for every staging task (a failed one re-raises in the loop)
         s_out.synchronize()
         cur.synchronize()
         _pinned_done("pipe_in", s_in)
+        if not ok:
+            _out_pool.give(buf)  # nothing in flight into it, and no result refers to it
     arr = np.asarray(_Lease(buf, (B, H, W)))
     for st in statuses:  # in plane order, as the batched path reports them
         raise_status(int(st.item()))

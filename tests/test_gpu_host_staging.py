@@ -152,5 +152,12 @@ def test_pipelined_planes_report_errors_in_channel_order():
     rng = np.random.default_rng(10)
     huge = ils.SmoothParams(ils.Charbonnier(0.8, 1e-4), 1e30, iters=3)
     planes = [rng.random((64, 96)) * 1e30 for _ in range(3)]
-    with pytest.raises(ils.NumericalError):
-        ils.smooth_color(ils.MultiImage(tuple(planes), ils.RGB), huge)
+    img = ils.MultiImage(tuple(planes), ils.RGB)
+    ils.smooth_color(img, PARAMS)  # a pooled buffer of this size exists
+    before = rt._out_pool.total
+    for _ in range(3):
+        with pytest.raises(ils.NumericalError):
+            ils.smooth_color(img, huge)
+    ok = ils.smooth_color(img, PARAMS)
+    assert ok.channels[0].shape == (64, 96)
+    assert rt._out_pool.total == before  # failed calls returned their result buffers
