@@ -888,21 +888,29 @@ def main():
                               "chunk's H2D queued as it lands; out: widened to f64 on the device (ils_convert), "
                               "one DMA into pooled pinned result planes")}
 
+    def leg(fn, *a):
+        # a secondary leg that raises (the same way on every rank) is reported
+        # in the line instead of losing the headline measurement taken above
+        try:
+            return fn(*a)
+        except Exception as e:  # noqa: BLE001
+            return {"error": f"{type(e).__name__}: {e}"[:300]}
+
     # ---- C1 / C2: gray frames (BASELINE.json configs[0..1])
     c1 = c2 = None
     if not args.no_gray:
-        c1 = gray_leg(args, world, rank, dev, barrier, max_over_ranks, 512, 512, "C1")
-        c2 = gray_leg(args, world, rank, dev, barrier, max_over_ranks, 1080, 1920, "C2")
+        c1 = leg(gray_leg, args, world, rank, dev, barrier, max_over_ranks, 512, 512, "C1")
+        c2 = leg(gray_leg, args, world, rank, dev, barrier, max_over_ranks, 1080, 1920, "C2")
 
     # ---- C4: 3840x2160 RGB video, 256 frames sharded over the ranks (BASELINE.json configs[3])
     c4 = None
     if not args.no_c4:
-        c4 = c4_leg(args, world, rank, dev, barrier, max_over_ranks)
+        c4 = leg(c4_leg, args, world, rank, dev, barrier, max_over_ranks)
 
     # ---- C5: one 7680x4320 RGB image, Welsch N=10 (BASELINE.json configs[4])
     c5 = None
     if not args.no_c5:
-        c5 = c5_leg(args, world, rank, local, dev, barrier, max_over_ranks)
+        c5 = leg(c5_leg, args, world, rank, local, dev, barrier, max_over_ranks)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
