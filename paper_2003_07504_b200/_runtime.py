@@ -260,12 +260,16 @@ _CHUNK_BYTES = int(float(os.environ.get("ILS_CHUNK_MB", "4")) * (1 << 20))
 _HOST_NARROW = os.environ.get("ILS_HOST_NARROW", "1") == "1"
 
 
+_pool_lock = threading.Lock()
+
+
 def _host_pool():
     global _pool
-    if _pool is None:
-        from concurrent.futures import ThreadPoolExecutor
+    with _pool_lock:
+        if _pool is None:
+            from concurrent.futures import ThreadPoolExecutor
 
-        _pool = ThreadPoolExecutor(max_workers=_HOST_THREADS, thread_name_prefix="ils-host")
+            _pool = ThreadPoolExecutor(max_workers=_HOST_THREADS, thread_name_prefix="ils-host")
     return _pool
 
 
