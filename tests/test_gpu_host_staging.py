@@ -161,3 +161,18 @@ def test_pipelined_planes_report_errors_in_channel_order():
     ok = ils.smooth_color(img, PARAMS)
     assert ok.channels[0].shape == (64, 96)
     assert rt._out_pool.total == before  # failed calls returned their result buffers
+
+
+def test_concurrent_callers_get_their_own_results():
+    # per-thread staging buffers and streams, a shared host pool and result pool
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(11)
+    imgs = [ils.MultiImage(tuple(rng.random((150, 256)) for _ in range(3)), ils.RGB) for _ in range(8)]
+    serial = [ils.smooth_color(im, PARAMS) for im in imgs]
+    with ThreadPoolExecutor(4) as ex:
+        for _ in range(2):
+            par = list(ex.map(lambda im: ils.smooth_color(im, PARAMS), imgs))
+            for a, b in zip(par, serial):
+                for c in range(3):
+                    assert np.array_equal(a.channels[c], b.channels[c])
