@@ -1923,11 +1923,53 @@ ils_status slab_row_t(const ils_plan* p, int mode, const T* f_ext, const cx<T>* 
   const dim3 grid(p->row_grid, 1);
   cudaError_t e;
   if constexpr (std::is_same<T, float>::value) {
+    // the rolling-band first / fused passes on the slab's rows (as launch_row;
+    // chunk rows for the slab height, one plane per launch)
+    if (p->roll_smem > 0 && (mode == MODE_F0 || mode == MODE_IT) && a.pen.kind != ILS_SOFT &&
+        !env_int("ILS_NO_ROLL", 0)) {
+      const long slots = (long)p->sms * std::min<long>(ILS_ROLL_MINB, (228 * 1024) / (p->roll_smem + 1024));
+      int R = 0;
+      double best = 1e300;
+      for (int r = 2; r <= p->Hl; ++r) {
+        const double cost = (double)(((p->Hl + r - 1) / r + slots - 1) / slots) * (r + 2);
+        if (cost < best * (1 - 1e-9)) {
+          best = cost;
+          R = r;
+        }
+      }
+      if (const int forced = env_int("ILS_ROLL_ROWS", 0)) R = std::min(forced, p->Hl);
+      if (R > 0) {
+        a.band = R;
+        const dim3 rgrid((p->Hl + R - 1) / R, 1);
+        switch (p->row_spec) {
+#define ILS_CASE(ID, ...)                                                                               \
+  case ID:                                                                                              \
+    if constexpr (ILS_ROW_SPEC_ROLL(ID)) {                                                              \
+      e = launch_row_roll_impl<RowSpec<ID>::type>(a, rgrid, p->roll_smem, p->roll_pf, s);              \
+      if (e != cudaSuccess) return fail(ILS_ECUDA, "slab row pass: %s", cudaGetErrorString(e));        \
+      return ILS_OK;                                                                                    \
+    }                                                                                                   \
+    break;
+          ILS_ROW_SPECS(ILS_CASE)
+#undef ILS_CASE
+          default:
+            break;
+        }
+        a.band = p->band;
+      }
+    }
+    // the final pass (no halo rows): its own rows per CTA, as launch_row
+    dim3 g2 = grid;
+    size_t smem = p->row_smem;
+    if (mode == MODE_FIN) {
+      a.band = p->fin_band;
+      g2 = dim3((p->Hl + a.band - 1) / a.band, 1);
+      smem = p->fin_smem;
+    }
     switch (p->row_spec) {
 #define ILS_CASE(ID, ...)                                                                                      \
   case ID:                                                                                                     \
-    e = launch_row_impl<float, true, RowSpec<ID>::type, ILS_ROW_SPEC_WIDE(ID)>(a, grid, p->row_threads,        \
-                                                                             p->row_smem, s);                 \
+    e = launch_row_impl<float, true, RowSpec<ID>::type, ILS_ROW_SPEC_WIDE(ID)>(a, g2, p->row_threads, smem, s); \
     if (e != cudaSuccess) return fail(ILS_ECUDA, "slab row pass: %s", cudaGetErrorString(e));                 \
     return ILS_OK;
       ILS_ROW_SPECS(ILS_CASE)

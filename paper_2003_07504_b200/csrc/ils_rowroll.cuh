@@ -103,15 +103,27 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   // FFT plan included, with generic loads)
   const cx<T>* Sin_b = IT ? A.Sin + (size_t)b * A.S_ps : nullptr;
   const long long S_rp = A.S_rp, f_rp = A.f_rp;
+  // slab plans (C5 over ranks): rows are not periodic (halo rows -1 and H are
+  // present) and spectrum rows move as the all-to-all blocks' column segments
+  const int nseg = A.sin_seg.n;
+  unsigned seg_bytes = 0;
+  for (int q = 0; q < nseg; ++q)
+    seg_bytes += (unsigned)(((A.sin_seg.c0[q + 1] - A.sin_seg.c0[q] + 1) & ~1) * sizeof(cx<T>));
+#define ROWY(y) (A.wrap ? wrapi((y), H) : (y))
   // one thread: TMA of row y (f for the first pass, the spectrum otherwise) into a slot
 #define ILS_ROLL_ISSUE(slot, y)                                                                                  \
   do {                                                                                                           \
-    if (IT) {                                                                                                    \
+    if (IT && nseg > 0) { /* slab plan: the row's P column segments from the all-to-all blocks */               \
+      mbar_expect_tx(&bars[slot], seg_bytes);                                                                    \
+      for (int q_ = 0; q_ < nseg; ++q_)                                                                          \
+        bulk_g2s(L.line(slot) + A.sin_seg.c0[q_], A.Sin + A.sin_seg.off[q_] + (long long)(y)*A.sin_seg.pitch[q_], \
+                 (unsigned)(((A.sin_seg.c0[q_ + 1] - A.sin_seg.c0[q_] + 1) & ~1) * sizeof(cx<T>)), &bars[slot]); \
+    } else if (IT) {                                                                                             \
       mbar_expect_tx(&bars[slot], spec_bytes);                                                                   \
-      bulk_g2s_hint(L.line(slot), Sin_b + (size_t)(y)*S_rp, spec_bytes, &bars[slot], l2_evict_first());         \
+      bulk_g2s_hint(L.line(slot), Sin_b + (long long)(y)*S_rp, spec_bytes, &bars[slot], l2_evict_first());      \
     } else {                                                                                                     \
       mbar_expect_tx(&bars[slot], (unsigned)(W * sizeof(T)));                                                    \
-      bulk_g2s(L.line(slot), fpl + (size_t)(y)*f_rp, (unsigned)(W * sizeof(T)), &bars[slot]);                    \
+      bulk_g2s(L.line(slot), fpl + (long long)(y)*f_rp, (unsigned)(W * sizeof(T)), &bars[slot]);                 \
     }                                                                                                            \
   } while (0)
   unsigned phase = 0;  // bit s: parity of the next completion of bars[s] (uniform over the CTA)
@@ -127,7 +139,7 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
 
   // ---------------- prologue: rows r0-1 and r0; mu_y of row r0-1
   if (tid == 0) {
-    ILS_ROLL_ISSUE(0, wrapi(r0 - 1, H));
+    ILS_ROLL_ISSUE(0, ROWY(r0 - 1));
     ILS_ROLL_ISSUE(1 % NS, r0);
   }
   if (NG == 1) {
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   int p = 1 % NS;   // slot of u_j
   {  // the first step's rows (and with PF the second step's)
     const int ahead = min((1 + PF) * NG, r1 - r0);
-    if (tid < ahead) ILS_ROLL_ISSUE((p + 1 + tid) % NS, wrapi(r0 + 1 + tid, H));
+    if (tid < ahead) ILS_ROLL_ISSUE((p + 1 + tid) % NS, ROWY(r0 + 1 + tid));
   }
   T chk = T(0);  // fma(x, 0, chk) turns NaN on any non-finite u of the chunk
   float2 chk2 = make_float2(0.f, 0.f);
@@ -259,10 +271,17 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
       }
       r2c_post<T>(z, FS::n, TwTab<T, WSMEM>{swreal}, g);
       if (g.rank == 0) {
-        bulk_s2g(A.Sout + (size_t)b * A.S_ps + (size_t)(j + i) * A.S_rp, z, spec_bytes);
+        if (A.sout_seg.n > 0) {  // slab plan: fused pack into the P all-to-all blocks
+          const SegRows& so = A.sout_seg;
+          for (int q = 0; q < so.n; ++q)
+            bulk_s2g(A.Sout + so.off[q] + (long long)(j + i) * so.pitch[q], z + so.c0[q],
+                     (unsigned)(((so.c0[q + 1] - so.c0[q] + 1) & ~1) * sizeof(cx<T>)));
+        } else {
+          bulk_s2g(A.Sout + (size_t)b * A.S_ps + (size_t)(j + i) * A.S_rp, z, spec_bytes);
+        }
         if (i < ngn) {  // full steps: slot (p + i) hosts row jn + 1 + i
           bulk_wait_reads();
-          ILS_ROLL_ISSUE(sl, wrapi(jn + 1 + i, H));
+          ILS_ROLL_ISSUE(sl, ROWY(jn + 1 + i));
         }
 #ifndef ILS_ROLL_NO_L2PF
         // one step further ahead, into L2 only (no shared memory to spare):
@@ -274,10 +293,10 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
 #endif
         const int y2 = jn + ILS_ROLL_L2PF_STEPS * NG + 1 + i;
         if (y2 <= r1) {
-          if (IT)
-            prefetch_l2(Sin_b + (size_t)wrapi(y2, H) * S_rp, spec_bytes);
-          else
-            prefetch_l2(fpl + (size_t)wrapi(y2, H) * f_rp, (unsigned)(W * sizeof(T)));
+          if (IT && nseg == 0)
+            prefetch_l2(Sin_b + (long long)ROWY(y2) * S_rp, spec_bytes);
+          else if (!IT)
+            prefetch_l2(fpl + (long long)ROWY(y2) * f_rp, (unsigned)(W * sizeof(T)));
         }
         if (IT && j + ILS_ROLL_L2PF_STEPS * NG + i < r1)
           prefetch_l2(fpl + (size_t)(j + ILS_ROLL_L2PF_STEPS * NG + i) * f_rp, (unsigned)(W * sizeof(T)));
@@ -292,6 +311,7 @@ __global__ void __launch_bounds__(kRowThreads, kRollBlocksOf<FS>) k_row_roll(con
   bulk_wait_reads();
 #undef ILS_ROLL_ISSUE
 #undef ILS_ROLL_LAND
+#undef ROWY
 }
 
 template <class FS>
