@@ -279,3 +279,15 @@ def test_application_params_validation():
         with pytest.raises(ValueError):
             ils.TonemapParams(base, **kw)
     ils.TonemapParams(base, lambdas=(1.0, 1.0, 1.0))
+
+
+def test_bench_pass_order_matches_the_header():
+    # include/ils_b200.h (ils_launch_pass): 0, 1, 2, 5, 6, 1, 2, 5, ..., ending with 3 or 7
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert bench.pass_order_of(4) == [0, 1, 2, 5, 6, 1, 2, 5, 7]
+    assert bench.pass_order_of(1) == [0, 1, 3]
+    assert bench.pass_order_of(3) == [0, 1, 2, 5, 6, 1, 3]
