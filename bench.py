@@ -264,7 +264,8 @@ def run_reference(args, rank):
 
 def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
     """C1 / C2 (BASELINE.json configs[0..1]): gray frames of h x w, Charbonnier p=0.8, lambda=1,
-    N=4; device frames/s over 2 lanes, 32 frames per step (one plane each), CUDA graph, max over ranks."""
+    N=4; device frames/s over 8 (512^2) or 4 (1080p) lanes, 32 frames per step (one plane each), CUDA graph,
+    max over ranks."""
     import torch
 
     import paper_2003_07504_b200 as ils
@@ -279,7 +280,11 @@ def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
     g.manual_seed(20240607 + rank)
     f = torch.rand((F, h, w), generator=g, device=dev)
     u = torch.empty_like(f)
-    lanes = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    # one plane per call leaves a 1080p pass at 180 row CTAs (a 512^2 one at
+    # 86) for 444 slots: more concurrent lanes fill the GPU (C1 2 / 8 lanes:
+    # 30.7k / 67.1k frames/s; C2 2 / 4 lanes: 13.1k / 18.0k; tools/gpu_gray_lanes.sh)
+    nl = int(os.environ.get("ILS_GRAY_LANES", "0")) or (8 if h * w <= 512 * 512 else 4)
+    lanes = [torch.cuda.Stream(device=dev) for _ in range(nl)]
     wss = [torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev) for _ in lanes]
     sts = [torch.empty(1, dtype=torch.int32, device=dev) for _ in lanes]
 
@@ -290,10 +295,10 @@ def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
     st_pp = torch.full((1,), _lib.STATUS_CLEAN, dtype=torch.int32, device=dev)
 
     def launches(s):
-        if not stagger:
-            lanes[1].wait_stream(s)
+        for ln_ in lanes[1:] if not stagger else lanes[2:]:
+            ln_.wait_stream(s)
         for k in range(F):
-            ln = k % 2
+            ln = k % nl
             if k == 0 and stagger:
                 for q, p in enumerate(order):
                     _lib.check(L.ils_launch_pass(plan.ptr, p, C.c_void_p(f[0].data_ptr()), C.c_void_p(u[0].data_ptr()),
@@ -305,9 +310,10 @@ def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
                         lanes[1].wait_event(ev)
                 continue
             _lib.check(L.ils_smooth(plan.ptr, C.c_void_p(f[k].data_ptr()), C.c_void_p(u[k].data_ptr()), h * w,
-                                    C.c_void_p(wss[ln].data_ptr()), C.c_void_p((s if ln == 0 else lanes[1]).cuda_stream),
+                                    C.c_void_p(wss[ln].data_ptr()), C.c_void_p((s if ln == 0 else lanes[ln]).cuda_stream),
                                     C.c_void_p(sts[ln].data_ptr()), None), "ils_smooth")
-        s.wait_stream(lanes[1])
+        for ln_ in lanes[1:]:
+            s.wait_stream(ln_)
 
     with torch.cuda.stream(lanes[0]):
         launches(lanes[0])
@@ -333,7 +339,7 @@ def gray_leg(args, world, rank, dev, barrier, max_over_ranks, h, w, label):
     peak, _ = peaks()
     bpf = bytes_per_frame(ITERS, h, w, 1)
     return {"workload": f"{label}: {w}x{h} gray ILS, Charbonnier p=0.8 eps=1e-4 lambda=1, 4 iters",
-            "value": round(fps, 1), "unit": "frames/s", "frames_per_step_per_gpu": F, "lanes": 2,
+            "value": round(fps, 1), "unit": "frames/s", "frames_per_step_per_gpu": F, "lanes": nl,
             "lane_stagger_passes": stagger,
             "whole_path": {"achieved": round(bpf * fps / world / 1e9, 1),
                            "frac": round(bpf * fps / world / 1e9 / peak, 4), "bytes_per_frame": bpf}}
